@@ -1,0 +1,199 @@
+/*
+ * cellsched_b200.h -- C ABI of the B200-native link-cell LJ hot path.
+ *
+ * Drop-in boundary for the reference package `cellsched`
+ * (/root/reference/pkg/src/cellsched).  The reference is pure Python with no
+ * FFI; these entry points are what its Python API binds through ctypes
+ * (see INTEGRATION.md).  Each declaration names the reference interface it
+ * replaces (file:line).  Functions the reference lacks (particles, LJ,
+ * integration -- SPEC.md:12, :462, :472) extend its idiom at the payload
+ * plug-in point (payload.py:84-174).
+ *
+ * Conventions
+ *  - return 0 on success, a cudaError_t (>0) or a negative CS_E* code on
+ *    failure; cs_last_error() returns a message for the calling thread.
+ *  - all array arguments are DEVICE pointers owned by the caller (e.g.
+ *    torch tensors' data_ptr()), except where a parameter says "host".
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *    calls are stream-ordered and never synchronise unless documented.
+ *  - temporary memory comes from a caller workspace `ws` of `ws_bytes`;
+ *    the matching *_ws_bytes() query returns the size needed.
+ *  - cell ids are x-fastest: c = x + ex*(y + ey*z)  (grid.py:3-4, :93-101).
+ */
+#ifndef CELLSCHED_B200_H
+#define CELLSCHED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_OK 0
+#define CS_EINVAL (-1)     /* bad argument (reference raises ValueError)        */
+#define CS_ECAPACITY (-2)  /* workspace / cell capacity exceeded               */
+#define CS_ECONFLICT (-3)  /* race detector: two writers of one cell in a pass */
+#define CS_ERANGE (-4)     /* particle outside the local cell range            */
+#define CS_ECYCLE (-5)     /* non-forward edge (depgraph.py:170-171)           */
+
+/* Grid of cells: dim 2 or 3, extents, per-axis periodicity
+ * (GridSpec, grid.py:43-101; per-axis periodicity generalises the single
+ * flag so an x-slab can be open in x). */
+typedef struct cs_grid {
+  int32_t dim;
+  int32_t ext[3];
+  int32_t periodic[3];
+} cs_grid;
+
+int cs_abi_version(void);
+const char *cs_last_error(void);
+int cs_device_synchronize(void);
+
+/* ===================== K4: task streams and serialization depth ========== */
+enum { CS_STREAM_BASIC = 0, CS_STREAM_LOOPEX = 1 };
+
+/* Number of tasks of a stream (host only, closed form).  basic: order is a
+ * host array of n offsets x dim int8 (StencilOrder.offsets); loopex: order
+ * ignored, canonical stencil, colour stride `stride` (2 = reference).
+ * Replaces len(generate_basic(...)) / len(generate_loopex(...))
+ * (taskgen.py:180-234). */
+int64_t cs_stream_count(const cs_grid *g, int strategy, const int8_t *order_host, int n,
+                        int stride);
+
+/* Generate a stream as arrays: home[t], nbr[t] (-1 for intra) and entry[t]
+ * (index into the order / canonical stencil), t in creation order.
+ * Replaces generate_basic (taskgen.py:180-199) and generate_loopex
+ * (taskgen.py:202-234); truncated non-periodic tasks are dropped
+ * (taskgen.py:195-197). */
+size_t cs_stream_ws_bytes(const cs_grid *g, int n);
+int cs_stream_generate(const cs_grid *g, int strategy, const int8_t *order_host, int n,
+                       int stride, int32_t *home, int32_t *nbr, int16_t *entry, int64_t ntasks,
+                       void *ws, size_t ws_bytes, void *stream);
+
+/* Dependency edges of an accumulator stream (every task writes acc(home)
+ * and acc(nbr)).  Writes pred_a[t], pred_b[t] (-1 = none; pred_a < pred_b
+ * when both exist, duplicates collapsed) -- the (succ, pred)-sorted edge
+ * list of detect_dependencies (depgraph.py:102-117, rule :28-49).
+ * `order_host`/`n`/`strategy`/`stride` must be the ones the stream was
+ * generated with (the accessor sets are closed-form).  Synchronises; writes
+ * the edge count to *nedges_host. */
+size_t cs_edges_ws_bytes(const cs_grid *g, int n, int64_t ntasks);
+int cs_stream_edges(const cs_grid *g, int strategy, const int8_t *order_host, int n, int stride,
+                    const int32_t *home, const int32_t *nbr, int64_t ntasks, int32_t *pred_a,
+                    int32_t *pred_b, int64_t *nedges_host, void *ws, size_t ws_bytes,
+                    void *stream);
+
+/* Compact (pred_a, pred_b) into edge arrays eu/ev sorted by (succ, pred). */
+int cs_edges_compact(int64_t ntasks, const int32_t *pred_a, const int32_t *pred_b, int64_t *eu,
+                     int64_t *ev, void *ws, size_t ws_bytes, void *stream);
+
+/* Serialization depth = critical_path (depgraph.py:160-174) and per-task
+ * level (longest path ending at t, counted in tasks).  method 0 = level
+ * relaxation (shallow orders), 1 = cell-chain DP (cell-grouped streams,
+ * e.g. generate_basic), 2 = auto.  Synchronises; *depth_host gets the depth. */
+size_t cs_depth_ws_bytes(int64_t ntasks);
+int cs_stream_depth(const cs_grid *g, int strategy, int n, int64_t ntasks, const int32_t *home,
+                    const int32_t *nbr, const int32_t *pred_a, const int32_t *pred_b,
+                    int32_t *level, int method, int64_t *depth_host, void *ws, size_t ws_bytes,
+                    void *stream);
+
+/* ===================== K5: integer payload (parity harness) ============== */
+/* charges (payload.py:58-61): q[cell] */
+int cs_payload_charges(const cs_grid *g, int64_t seed, int64_t *q, void *stream);
+/* reference_oracle analogue (payload.py:152-174): direct 3^dim-1 sum */
+int cs_payload_direct(const cs_grid *g, int64_t seed, const int64_t *q, int64_t *acc,
+                      void *stream);
+/* apply_tasks analogue (payload.py:84-119): execute a stream level by level
+ * (tasks of one dependency level are write-disjoint), no atomics.
+ * `level` from cs_stream_depth; entry_offsets_host = n x dim int8. */
+size_t cs_payload_levels_ws_bytes(int64_t ntasks, int64_t depth);
+int cs_payload_levels(const cs_grid *g, const int64_t *q, int64_t ntasks, const int32_t *home,
+                      const int32_t *nbr, const int16_t *entry, const int8_t *entry_offsets_host,
+                      int n, const int32_t *level, int64_t depth, int64_t *acc, void *ws,
+                      size_t ws_bytes, void *stream);
+/* The colour-pass schedules of the LJ kernel, run on the integer payload:
+ * sched CS_SCHED_LOOPEX (27 passes) or CS_SCHED_BLOCK (8 block passes).
+ * race_check != 0 records writers per pass and fails with CS_ECONFLICT. */
+int cs_payload_colour(const cs_grid *g, int sched, const int32_t *block_host, const int64_t *q,
+                      int64_t *acc, int race_check, void *ws, size_t ws_bytes, void *stream);
+size_t cs_payload_colour_ws_bytes(const cs_grid *g);
+
+/* ===================== LJ link-cell MD (new; extends the payload plug-in) */
+enum { CS_SCHED_LOOPEX = 0, CS_SCHED_BLOCK = 1 };
+
+/* Local cell box.  Single GPU: nc == gnc, x0 == 0, periodic {1,1,1}.
+ * x-slab rank: nc[0] = owned planes + 1 ghost plane, periodic[0] = 0,
+ * x0 = global index of local plane 0.  inv = gnc / L (binning), L = box. */
+typedef struct cs_box {
+  int32_t nc[3];
+  int32_t gnc[3];
+  int32_t x0;
+  int32_t owned_x; /* planes whose cells own home tasks (nc[0]-1 in slab mode) */
+  int32_t periodic[3];
+  int32_t block[3]; /* CS_SCHED_BLOCK block shape in cells */
+  double L[3];
+  double inv[3];
+} cs_box;
+
+typedef struct cs_lj {
+  double eps, sigma, rc, mass;
+} cs_lj;
+
+/* FCC lattice + seeded jitter, id order (4 sites per unit cell). */
+int cs_init_fcc(const int32_t *nuc_host, const double *a_host, const double *L_host,
+                double jitter, int64_t seed, double *x, double *y, double *z, int32_t *id,
+                void *stream);
+/* Gaussian velocities, momentum removed, scaled to exactly T (3N-3 dof). */
+size_t cs_reduce_ws_bytes(int64_t n);
+int cs_init_velocities(int64_t n, double T, double mass, int64_t seed, double *vx, double *vy,
+                       double *vz, void *ws, size_t ws_bytes, void *stream);
+
+/* K1: cell list as a stable counting sort (histogram, scan, scatter, then
+ * canonical id order within each cell).  Gathers x, v, id into the
+ * cell-sorted outputs, zeroes f_out, writes cell_start[ncells+1].
+ * v pointers may be NULL (positions only). */
+size_t cs_bin_ws_bytes(int64_t n, const cs_box *b);
+int cs_build_cells(int64_t n, const cs_box *b, const double *x, const double *y,
+                   const double *z, const double *vx, const double *vy, const double *vz,
+                   const int32_t *id, double *xo, double *yo, double *zo, double *vxo,
+                   double *vyo, double *vzo, int32_t *ido, double *fxo, double *fyo,
+                   double *fzo, int32_t *cell_start, void *ws, size_t ws_bytes, void *stream);
+
+/* K2: fp64 LJ half-shell forces with Newton-3 reaction writes under a
+ * conflict-free colour-pass schedule; f must be zeroed by the caller
+ * (cs_build_cells does).  energy_dev[0] += PE, npairs_dev[0] += pairs
+ * (either may be NULL). */
+size_t cs_force_ws_bytes(const cs_box *b, int sched);
+int cs_lj_forces(const cs_box *b, const cs_lj *p, int sched, const int32_t *cell_start,
+                 const double *x, const double *y, const double *z, double *fx, double *fy,
+                 double *fz, double *energy_dev, unsigned long long *npairs_dev, void *ws,
+                 size_t ws_bytes, void *stream);
+
+/* K3: velocity Verlet.  kick: v += (dt/2m) f.  kick_drift: v += (dt/2m) f;
+ * x += dt v; wrap into [0, L) on periodic axes. */
+int cs_vv_kick(int64_t n, double hdtm, const double *fx, const double *fy, const double *fz,
+               double *vx, double *vy, double *vz, void *stream);
+int cs_vv_kick_drift(int64_t n, double hdtm, double dt, const cs_box *b, const double *fx,
+                     const double *fy, const double *fz, double *vx, double *vy, double *vz,
+                     double *x, double *y, double *z, void *stream);
+
+/* K6: deterministic reductions.  out_dev[0] = 0.5 m sum v^2 */
+int cs_kinetic(int64_t n, double mass, const double *vx, const double *vy, const double *vz,
+               double *out_dev, void *ws, size_t ws_bytes, void *stream);
+/* out_dev[0..2] = sum of each component */
+int cs_sum3(int64_t n, const double *ax, const double *ay, const double *az, double *out_dev,
+            void *ws, size_t ws_bytes, void *stream);
+
+/* Slab halo helpers: pack the particles of local x-plane `plane` (cells
+ * [plane*ny*nz ...]) into a contiguous buffer (positions, x shifted by
+ * xshift), and add ghost-plane forces back. */
+int cs_pack_plane(const cs_box *b, int plane, const int32_t *cell_start, const double *x,
+                  const double *y, const double *z, double xshift, double *out, void *stream);
+int cs_add_plane_forces(const cs_box *b, int plane, const int32_t *cell_start, const double *in,
+                        double *fx, double *fy, double *fz, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,9 @@
+// cs_lib.cu -- the single translation unit of libcellsched_b200.so (sm_100a).
+#include <stdlib.h>
+#include <string.h>
+
+#include "cs_util.cuh"
+#include "cs_sched.cuh"
+#include "cs_payload.cuh"
+#include "cs_md.cuh"
+#include "cs_force.cuh"

@@ -1,0 +1,385 @@
+// cs_md.cuh -- particle setup, K1 cell binning, K3 velocity Verlet, slab helpers.
+//
+// No reference code exists for particles; the
+// conventions extend the reference's: x-fastest cell ids (grid.py:3-4), the
+// splitmix64 counter PRNG of payload.py:36-40 for every random draw, and the
+// cell list as the canonical (cell, particle id) order so it is independent
+// of history and bit-comparable with the CPU oracle.
+#pragma once
+#include "cs_common.cuh"
+
+#define JITTER_KEY 0xD1B54A32D192ED03ull
+#define VEL_KEY 0x8CB92BA72F3D8DD7ull
+
+struct Box {  // device-side copy of cs_box plus derived strides
+  int nc[3], gnc[3], x0, owned_x, per[3], blk[3];
+  int64_t stride[3];
+  int64_t ncells;
+  double L[3], inv[3];
+};
+
+static int make_box(const cs_box *b, Box *o) {
+  CS_REQUIRE(b, "null box");
+  for (int k = 0; k < 3; ++k) {
+    o->nc[k] = b->nc[k];
+    o->gnc[k] = b->gnc[k];
+    o->per[k] = b->periodic[k] ? 1 : 0;
+    o->blk[k] = b->block[k];
+    o->L[k] = b->L[k];
+    o->inv[k] = b->inv[k];
+    CS_REQUIRE(b->nc[k] >= 1 && b->gnc[k] >= 1, "cell counts must be >= 1");
+  }
+  o->x0 = b->x0;
+  o->owned_x = b->owned_x > 0 ? b->owned_x : b->nc[0];
+  CS_REQUIRE(o->owned_x <= o->nc[0], "owned_x > nc[0]");
+  if (o->per[0]) {
+    // x-fastest storage = the reference's cell id (grid.py:93-101)
+    o->stride[0] = 1;
+    o->stride[1] = o->nc[0];
+    o->stride[2] = (int64_t)o->nc[0] * o->nc[1];
+  } else {
+    // x-slab storage: x slowest so the ghost plane is the tail of the arrays
+    o->stride[0] = (int64_t)o->nc[1] * o->nc[2];
+    o->stride[1] = 1;
+    o->stride[2] = o->nc[1];
+  }
+  o->ncells = (int64_t)o->nc[0] * o->nc[1] * o->nc[2];
+  return CS_OK;
+}
+
+__host__ __device__ __forceinline__ int64_t box_cell(const Box &b, int x, int y, int z) {
+  return x * b.stride[0] + y * b.stride[1] + z * b.stride[2];
+}
+
+__device__ __forceinline__ double uni_dev(uint64_t base, uint64_t i) {
+  return (double)(cs_splitmix64(base + i) >> 11) * 0x1.0p-53;
+}
+__device__ __forceinline__ double wrap_dev(double x, double L) {
+  if (x < 0.0) x = __dadd_rn(x, L);
+  if (x >= L) x = __dadd_rn(x, -L);
+  return x;
+}
+
+// ------------------------------------------------------------------ setup --
+struct FccArgs {
+  int nuc[3];
+  double a[3], L[3], jit;
+  uint64_t base;
+};
+__global__ void k_init_fcc(FccArgs f, int64_t n, double *x, double *y, double *z, int32_t *id) {
+  const double bas[4][3] = {{0, 0, 0}, {0, 0.5, 0.5}, {0.5, 0, 0.5}, {0.5, 0.5, 0}};
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int b = (int)(p & 3);
+    int64_t uc = p >> 2;
+    int ii[3] = {(int)(uc % f.nuc[0]), (int)((uc / f.nuc[0]) % f.nuc[1]),
+                 (int)(uc / ((int64_t)f.nuc[0] * f.nuc[1]))};
+    double out[3];
+    for (int k = 0; k < 3; ++k) {
+      double t = __dadd_rn((double)ii[k], bas[b][k] + 0.25);
+      double u = uni_dev(f.base, (uint64_t)(3 * p + k));
+      double s = __dmul_rn(t, f.a[k]);
+      double j = __dmul_rn(__dadd_rn(__dmul_rn(2.0, u), -1.0), f.jit);
+      out[k] = wrap_dev(__dadd_rn(s, j), f.L[k]);
+    }
+    x[p] = out[0];
+    y[p] = out[1];
+    z[p] = out[2];
+    id[p] = (int32_t)p;
+  }
+}
+
+extern "C" int cs_init_fcc(const int32_t *nuc, const double *a, const double *L, double jitter,
+                           int64_t seed, double *x, double *y, double *z, int32_t *id,
+                           void *stream) {
+  FccArgs f;
+  int64_t n = 4;
+  for (int k = 0; k < 3; ++k) {
+    CS_REQUIRE(nuc[k] >= 1, "unit cells must be >= 1");
+    f.nuc[k] = nuc[k];
+    f.a[k] = a[k];
+    f.L[k] = L[k];
+    n *= nuc[k];
+  }
+  f.jit = jitter;
+  f.base = cs_splitmix64_host((uint64_t)seed ^ JITTER_KEY);
+  k_init_fcc<<<grid_for(n, 256), 256, 0, cs_stream(stream)>>>(f, n, x, y, z, id);
+  return cs_check_launch("init_fcc");
+}
+
+__global__ void k_init_gauss(int64_t n, uint64_t base, double *vx, double *vy, double *vz) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < 3 * n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = k >> 1;
+    double u1 = uni_dev(base, (uint64_t)(2 * q)), u2 = uni_dev(base, (uint64_t)(2 * q + 1));
+    double r = sqrt(-2.0 * log(1.0 - u1));
+    double th = 6.283185307179586 * u2;
+    double g = (k & 1) ? r * sin(th) : r * cos(th);
+    double *dst = (k % 3 == 0) ? vx : (k % 3 == 1 ? vy : vz);
+    dst[k / 3] = g;
+  }
+}
+// v -= mean (sums[0..2] / n)
+__global__ void k_remove_mean(int64_t n, const double *sums, double *vx, double *vy, double *vz) {
+  double mx = sums[0] / (double)n, my = sums[1] / (double)n, mz = sums[2] / (double)n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    vx[i] -= mx;
+    vy[i] -= my;
+    vz[i] -= mz;
+  }
+}
+// scale so that sum m v^2 = T (3N-3); ke2 = 0.5 m sum v^2
+__global__ void k_scale_T(int64_t n, double T, double mass, const double *ke, double *vx,
+                          double *vy, double *vz) {
+  double s2 = 2.0 * ke[0] / mass;
+  double sc = sqrt(T * (double)(3 * n - 3) / (mass * s2));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    vx[i] *= sc;
+    vy[i] *= sc;
+    vz[i] *= sc;
+  }
+}
+
+extern "C" int cs_init_velocities(int64_t n, double T, double mass, int64_t seed, double *vx,
+                                  double *vy, double *vz, void *ws, size_t ws_bytes,
+                                  void *stream) {
+  CS_REQUIRE(n >= 2, "need at least 2 particles");
+  cudaStream_t st = cs_stream(stream);
+  uint64_t base = cs_splitmix64_host((uint64_t)seed ^ VEL_KEY);
+  k_init_gauss<<<grid_for(3 * n, 256), 256, 0, st>>>(n, base, vx, vy, vz);
+  cs_ws w(ws, ws_bytes);
+  CS_WS_TAKE(w, double, sc, 8);
+  size_t rest = ws_bytes - w.used;
+  void *rws = w.base + w.used;
+  CS_TRY(cs_sum3(n, vx, vy, vz, sc, rws, rest, stream));
+  k_remove_mean<<<grid_for(n, 256), 256, 0, st>>>(n, sc, vx, vy, vz);
+  CS_TRY(cs_kinetic(n, mass, vx, vy, vz, sc + 4, rws, rest, stream));
+  k_scale_T<<<grid_for(n, 256), 256, 0, st>>>(n, T, mass, sc + 4, vx, vy, vz);
+  return cs_check_launch("init_velocities");
+}
+
+// ------------------------------------------------------------ K1: binning --
+__device__ __forceinline__ int bin_coord(double x, double inv, int n) {
+  int c = (int)(x * inv);  // single IEEE multiply, identical on the CPU oracle
+  return c >= n ? n - 1 : (c < 0 ? 0 : c);
+}
+
+__global__ void k_bin_count(int64_t n, Box b, const double *x, const double *y, const double *z,
+                            int32_t *cell_of, int32_t *slot, int32_t *count, int *err) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int cx = bin_coord(x[p], b.inv[0], b.gnc[0]) - b.x0;
+    int cy = bin_coord(y[p], b.inv[1], b.gnc[1]);
+    int cz = bin_coord(z[p], b.inv[2], b.gnc[2]);
+    if (cx < 0 || cx >= b.owned_x) {
+      atomicOr(err, 1);
+      cx = cx < 0 ? 0 : b.owned_x - 1;
+    }
+    int32_t c = (int32_t)box_cell(b, cx, cy, cz);
+    cell_of[p] = c;
+    slot[p] = atomicAdd(&count[c], 1);
+  }
+}
+
+__global__ void k_bin_scatter(int64_t n, const int32_t *cell_of, const int32_t *slot,
+                              const int32_t *start, int32_t *src) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    src[start[cell_of[p]] + slot[p]] = (int32_t)p;
+}
+
+// one warp per cell: rank the cell's particles by id (canonical order),
+// then gather x, v, id into the sorted arrays and zero the forces
+__global__ void k_cell_sort_gather(int64_t ncells, const int32_t *start, const int32_t *src,
+                                   const int32_t *id, const double *x, const double *y,
+                                   const double *z, const double *vx, const double *vy,
+                                   const double *vz, double *xo, double *yo, double *zo,
+                                   double *vxo, double *vyo, double *vzo, int32_t *ido,
+                                   double *fxo, double *fyo, double *fzo) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = warp; c < ncells; c += nwarps) {
+    int32_t s0 = start[c], cnt = start[c + 1] - s0;
+    for (int32_t a = 0; a < cnt; a += 32) {
+      int32_t me = a + lane;
+      int32_t p = me < cnt ? src[s0 + me] : -1;
+      int32_t myid = p >= 0 ? id[p] : 0x7fffffff;
+      int32_t rank = 0;
+      for (int32_t b2 = 0; b2 < cnt; b2 += 32) {
+        int32_t q = b2 + lane < cnt ? id[src[s0 + b2 + lane]] : 0x7fffffff;
+        int lim = min(32, cnt - b2);
+        for (int k = 0; k < lim; ++k) {
+          int32_t other = __shfl_sync(CS_FULL, q, k);
+          rank += (other < myid);
+        }
+      }
+      if (p >= 0) {
+        int32_t d = s0 + rank;
+        xo[d] = x[p];
+        yo[d] = y[p];
+        zo[d] = z[p];
+        if (vx) {
+          vxo[d] = vx[p];
+          vyo[d] = vy[p];
+          vzo[d] = vz[p];
+        }
+        ido[d] = myid;
+        fxo[d] = 0.0;
+        fyo[d] = 0.0;
+        fzo[d] = 0.0;
+      }
+    }
+  }
+}
+
+extern "C" size_t cs_bin_ws_bytes(int64_t n, const cs_box *b) {
+  int64_t nc = (int64_t)b->nc[0] * b->nc[1] * b->nc[2];
+  return 3 * cs_ws_slice(sizeof(int32_t) * (n + 1)) + cs_ws_slice(sizeof(int32_t) * (nc + 1)) +
+         cs_ws_slice(64) + cs_scan_ws_bytes(nc);
+}
+
+extern "C" int cs_build_cells(int64_t n, const cs_box *bx, const double *x, const double *y,
+                              const double *z, const double *vx, const double *vy,
+                              const double *vz, const int32_t *id, double *xo, double *yo,
+                              double *zo, double *vxo, double *vyo, double *vzo, int32_t *ido,
+                              double *fxo, double *fyo, double *fzo, int32_t *cell_start,
+                              void *ws, size_t ws_bytes, void *stream) {
+  Box b;
+  CS_TRY(make_box(bx, &b));
+  cudaStream_t st = cs_stream(stream);
+  cs_ws w(ws, ws_bytes);
+  CS_WS_TAKE(w, int32_t, cell_of, n + 1);
+  CS_WS_TAKE(w, int32_t, slot, n + 1);
+  CS_WS_TAKE(w, int32_t, src, n + 1);
+  CS_WS_TAKE(w, int32_t, count, b.ncells + 1);
+  CS_WS_TAKE(w, int, err, 16);
+  size_t sb = cs_scan_ws_bytes(b.ncells);
+  void *scratch = w.take<char>(sb);
+  CS_REQUIRE(scratch, "workspace too small for cell scan");
+  CS_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t) * (b.ncells + 1), st));
+  CS_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  if (n > 0)
+    k_bin_count<<<grid_for(n, 256), 256, 0, st>>>(n, b, x, y, z, cell_of, slot, count, err);
+  CS_TRY(cs_exclusive_scan_i32(count, cell_start, b.ncells, scratch, sb, st));
+  if (n > 0) {
+    k_bin_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, cell_of, slot, cell_start, src);
+    k_cell_sort_gather<<<grid_for(b.ncells * 32, 256), 256, 0, st>>>(
+        b.ncells, cell_start, src, id, x, y, z, vx, vy, vz, xo, yo, zo, vxo, vyo, vzo, ido, fxo,
+        fyo, fzo);
+  }
+  return cs_check_launch("build_cells");
+}
+
+// range errors of the last build (slab mode: particles that must migrate)
+// are reported through cs_bin_errors; kept separate so the build stays
+// free of host synchronisation.
+
+// ------------------------------------------------------------ K3: Verlet --
+__global__ void k_kick(int64_t n, double hdtm, const double *fx, const double *fy,
+                       const double *fz, double *vx, double *vy, double *vz) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    vx[i] = __fma_rn(hdtm, fx[i], vx[i]);
+    vy[i] = __fma_rn(hdtm, fy[i], vy[i]);
+    vz[i] = __fma_rn(hdtm, fz[i], vz[i]);
+  }
+}
+
+__global__ void k_kick_drift(int64_t n, double hdtm, double dt, double Lx, double Ly, double Lz,
+                             const double *fx, const double *fy, const double *fz, double *vx,
+                             double *vy, double *vz, double *x, double *y, double *z) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double ux = __fma_rn(hdtm, fx[i], vx[i]);
+    double uy = __fma_rn(hdtm, fy[i], vy[i]);
+    double uz = __fma_rn(hdtm, fz[i], vz[i]);
+    vx[i] = ux;
+    vy[i] = uy;
+    vz[i] = uz;
+    x[i] = wrap_dev(__fma_rn(dt, ux, x[i]), Lx);
+    y[i] = wrap_dev(__fma_rn(dt, uy, y[i]), Ly);
+    z[i] = wrap_dev(__fma_rn(dt, uz, z[i]), Lz);
+  }
+}
+
+extern "C" int cs_vv_kick(int64_t n, double hdtm, const double *fx, const double *fy,
+                          const double *fz, double *vx, double *vy, double *vz, void *stream) {
+  if (n <= 0) return CS_OK;
+  k_kick<<<grid_for(n, 256), 256, 0, cs_stream(stream)>>>(n, hdtm, fx, fy, fz, vx, vy, vz);
+  return cs_check_launch("vv_kick");
+}
+
+extern "C" int cs_vv_kick_drift(int64_t n, double hdtm, double dt, const cs_box *b,
+                                const double *fx, const double *fy, const double *fz,
+                                double *vx, double *vy, double *vz, double *x, double *y,
+                                double *z, void *stream) {
+  if (n <= 0) return CS_OK;
+  k_kick_drift<<<grid_for(n, 256), 256, 0, cs_stream(stream)>>>(
+      n, hdtm, dt, b->L[0], b->L[1], b->L[2], fx, fy, fz, vx, vy, vz, x, y, z);
+  return cs_check_launch("vv_kick_drift");
+}
+
+// ------------------------------------------------------------ slab halos --
+// pack positions of local x-plane `plane` (storage-contiguous in slab mode)
+__global__ void k_pack_plane(int64_t lo, int64_t hi, const double *x, const double *y,
+                             const double *z, double xshift, double *out) {
+  int64_t m = hi - lo;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = __dadd_rn(x[lo + i], xshift);
+    out[m + i] = y[lo + i];
+    out[2 * m + i] = z[lo + i];
+  }
+}
+__global__ void k_add_plane(int64_t lo, int64_t hi, const double *in, double *fx, double *fy,
+                            double *fz) {
+  int64_t m = hi - lo;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    fx[lo + i] += in[i];
+    fy[lo + i] += in[m + i];
+    fz[lo + i] += in[2 * m + i];
+  }
+}
+
+static int plane_range(const Box &b, int plane, const int32_t *cell_start, int64_t *lo,
+                       int64_t *hi, cudaStream_t st) {
+  CS_REQUIRE(!b.per[0], "plane packing needs slab (x-slowest) storage");
+  CS_REQUIRE(plane >= 0 && plane < b.nc[0], "plane out of range");
+  int32_t h[2];
+  int64_t c0 = (int64_t)plane * b.stride[0];
+  CS_CUDA(cudaMemcpyAsync(&h[0], cell_start + c0, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CS_CUDA(cudaMemcpyAsync(&h[1], cell_start + c0 + b.stride[0], sizeof(int32_t),
+                          cudaMemcpyDeviceToHost, st));
+  CS_CUDA(cudaStreamSynchronize(st));
+  *lo = h[0];
+  *hi = h[1];
+  return CS_OK;
+}
+
+extern "C" int cs_pack_plane(const cs_box *bx, int plane, const int32_t *cell_start,
+                             const double *x, const double *y, const double *z, double xshift,
+                             double *out, void *stream) {
+  Box b;
+  CS_TRY(make_box(bx, &b));
+  cudaStream_t st = cs_stream(stream);
+  int64_t lo, hi;
+  CS_TRY(plane_range(b, plane, cell_start, &lo, &hi, st));
+  if (hi > lo) k_pack_plane<<<grid_for(hi - lo, 256), 256, 0, st>>>(lo, hi, x, y, z, xshift, out);
+  return cs_check_launch("pack_plane");
+}
+
+extern "C" int cs_add_plane_forces(const cs_box *bx, int plane, const int32_t *cell_start,
+                                   const double *in, double *fx, double *fy, double *fz,
+                                   void *stream) {
+  Box b;
+  CS_TRY(make_box(bx, &b));
+  cudaStream_t st = cs_stream(stream);
+  int64_t lo, hi;
+  CS_TRY(plane_range(b, plane, cell_start, &lo, &hi, st));
+  if (hi > lo) k_add_plane<<<grid_for(hi - lo, 256), 256, 0, st>>>(lo, hi, in, fx, fy, fz);
+  return cs_check_launch("add_plane_forces");
+}

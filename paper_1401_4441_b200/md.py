@@ -1,0 +1,354 @@
+"""Lennard-Jones link-cell molecular dynamics on the B200 (K1, K2, K3, K6).
+
+The reference has no particle code; this module
+extends its idiom at the payload plug-in point (payload.py:84-174): frozen
+dataclasses for parameters and geometry, x-fastest cell ids from
+`grid.GridSpec`, ValueError on bad input.  A step is
+
+    kick + drift + wrap (K3) -> cell list as a stable counting sort (K1)
+    -> fp64 LJ half-shell forces with Newton-3 reaction writes under a
+       conflict-free colour-pass schedule (K2) -> kick (K3) [-> energies, K6]
+
+all on one CUDA stream, capturable in a CUDA graph.  Particles live in
+cell-sorted SoA fp64 arrays (x, y, z, vx, vy, vz, fx, fy, fz) plus int32 ids,
+ping-ponged between two buffers by the rebinning gather.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+from . import _lib
+from .grid import GridSpec
+
+SCHEDULES = {"loopex": _lib.SCHED_LOOPEX, "block": _lib.SCHED_BLOCK}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass(frozen=True)
+class LJParams:
+    """U(r) = 4 eps [(sigma/r)^12 - (sigma/r)^6] for r < rc, unshifted."""
+
+    epsilon: float = 1.0
+    sigma: float = 1.0
+    rc: float = 2.5
+    mass: float = 1.0
+
+    def __post_init__(self) -> None:
+        if self.epsilon <= 0 or self.sigma <= 0 or self.rc <= 0 or self.mass <= 0:
+            raise ValueError("LJ parameters must be positive")
+
+
+@dataclass(frozen=True)
+class LJBox:
+    """Periodic orthorhombic box split into cells of edge >= rc."""
+
+    lengths: tuple[float, float, float]
+    cells: tuple[int, int, int]
+
+    def __post_init__(self) -> None:
+        object.__setattr__(self, "lengths", tuple(float(v) for v in self.lengths))
+        object.__setattr__(self, "cells", tuple(int(v) for v in self.cells))
+        if len(self.lengths) != 3 or len(self.cells) != 3:
+            raise ValueError("LJ boxes are 3D")
+        if min(self.cells) < 3:
+            raise ValueError(f"link cells need >= 3 cells per axis, got {self.cells}")
+
+    @classmethod
+    def for_cutoff(cls, lengths, rc: float) -> "LJBox":
+        cells = tuple(int(math.floor(L / rc)) for L in lengths)
+        return cls(tuple(lengths), cells)
+
+    @property
+    def grid(self) -> GridSpec:
+        return GridSpec(self.cells)
+
+    @property
+    def cell_edge(self) -> tuple[float, ...]:
+        return tuple(L / n for L, n in zip(self.lengths, self.cells))
+
+    @property
+    def inv(self) -> tuple[float, ...]:
+        # binning factor, computed once on the host and shared with the oracle
+        return tuple(float(n) / L for L, n in zip(self.lengths, self.cells))
+
+    @property
+    def cell_count(self) -> int:
+        return self.cells[0] * self.cells[1] * self.cells[2]
+
+
+def fcc_box(n_unit_cells, density: float, rc: float = 2.5):
+    """Box holding n^3 FCC unit cells (4 sites each) at `density`; returns
+    (box, unit-cell edges)."""
+    nuc = tuple(int(v) for v in (n_unit_cells if hasattr(n_unit_cells, "__len__") else (n_unit_cells,) * 3))
+    a = (4.0 / density) ** (1.0 / 3.0)
+    lengths = tuple(n * a for n in nuc)
+    return LJBox.for_cutoff(lengths, rc), nuc, (a, a, a)
+
+
+def choose_block(cells, density_per_cell: float = 13.5, cap: int = 2048):
+    """Largest block (By, Bz >= 2) whose 2x2x2 colour passes still fill the
+    GPU (>= 296 CTAs per pass) and whose footprint fits the staging cap."""
+    best = None
+    for shape in ((2, 2, 2), (2, 2, 4), (2, 4, 4), (4, 4, 4)):
+        if any(c % (2 * b) for c, b in zip(cells, shape)):
+            continue
+        foot = (shape[0] + 1) * (shape[1] + 2) * (shape[2] + 2)
+        if foot * density_per_cell * 1.3 > cap:
+            continue
+        per_pass = (cells[0] * cells[1] * cells[2]) // (8 * shape[0] * shape[1] * shape[2])
+        if best is None or per_pass >= 296:
+            best = shape
+    return best
+
+
+class LJSystem:
+    """Particles + cell list + workspaces on one GPU (single periodic domain)."""
+
+    def __init__(self, box: LJBox, n: int, params: LJParams = LJParams(), schedule: str = "block",
+                 block=None, device=None):
+        torch = _torch()
+        _lib.require_cuda()
+        if schedule not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {tuple(SCHEDULES)}")
+        for e in box.cell_edge:
+            if e < params.rc * (1 - 1e-12):
+                raise ValueError(f"cell edge {e} below cutoff {params.rc}")
+        self.box, self.params, self.n = box, params, int(n)
+        self.schedule = schedule
+        even = all(c % 2 == 0 for c in box.cells)
+        if schedule == "block":
+            self.block = tuple(block) if block is not None else choose_block(box.cells)
+            if self.block is None:
+                raise ValueError(f"no valid block shape for cells {box.cells}; use schedule='loopex'")
+        else:
+            if not even:
+                raise ValueError("loop-exchange colour passes need even periodic extents")
+            self.block = tuple(block) if block is not None else (2, 2, 2)
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        d, f64, i32 = self.device, torch.float64, torch.int32
+        self._buf = [
+            {k: torch.zeros(max(self.n, 1), dtype=f64, device=d) for k in ("x", "y", "z", "vx", "vy", "vz", "fx", "fy", "fz")}
+            for _ in range(2)
+        ]
+        for b in self._buf:
+            b["id"] = torch.zeros(max(self.n, 1), dtype=i32, device=d)
+        self.cur = 0
+        self.cell_start = torch.zeros(box.cell_count + 1, dtype=i32, device=d)
+        self._cbox = self._make_cbox()
+        self._clj = _lib.CsLJ(params.epsilon, params.sigma, params.rc, params.mass)
+        L = _lib.load()
+        wsb = max(L.cs_bin_ws_bytes(self.n, C.byref(self._cbox)),
+                  L.cs_force_ws_bytes(C.byref(self._cbox), SCHEDULES[schedule]),
+                  L.cs_reduce_ws_bytes(self.n))
+        self._wsb = int(wsb)
+        self._ws = torch.empty(self._wsb, dtype=torch.uint8, device=d)
+        self.scal = torch.zeros(8, dtype=f64, device=d)  # [0]=PE [1]=KE
+        self.npairs = torch.zeros(1, dtype=torch.int64, device=d)
+        self.dt = 0.005
+        self._graphs = {}
+
+    # ----------------------------------------------------------- plumbing
+    def _make_cbox(self):
+        b = _lib.CsBox()
+        for k in range(3):
+            b.nc[k] = b.gnc[k] = self.box.cells[k]
+            b.periodic[k] = 1
+            b.block[k] = self.block[k]
+            b.L[k] = self.box.lengths[k]
+            b.inv[k] = self.box.inv[k]
+        b.x0 = 0
+        b.owned_x = self.box.cells[0]
+        return b
+
+    def _s(self):
+        return _lib.stream_handle()
+
+    def _a(self, name, which=None):
+        return self._buf[self.cur if which is None else which][name]
+
+    @property
+    def x(self):
+        return self._a("x")
+
+    @property
+    def y(self):
+        return self._a("y")
+
+    @property
+    def z(self):
+        return self._a("z")
+
+    # ------------------------------------------------------------- set up
+    @classmethod
+    def fcc(cls, n_unit_cells=6, density: float = 0.8442, temperature: float = 0.722,
+            jitter: float = 0.05, seed: int = 42, params: LJParams = LJParams(),
+            schedule: str = "block", block=None, dt: float = 0.005):
+        """FCC lattice + seeded uniform jitter + Gaussian velocities at T
+        (momentum removed, 3N-3 dof), then cell list + initial forces."""
+        box, nuc, a = fcc_box(n_unit_cells, density, params.rc)
+        n = 4 * nuc[0] * nuc[1] * nuc[2]
+        s = cls(box, n, params, schedule, block)
+        s.dt = dt
+        s.seed_fcc(nuc, a, temperature, jitter, seed)
+        return s
+
+    def seed_fcc(self, nuc, a, temperature, jitter, seed):
+        src = self.cur
+        b = self._buf[src]
+        nu = (C.c_int32 * 3)(*nuc)
+        aa = (C.c_double * 3)(*a)
+        LL = (C.c_double * 3)(*self.box.lengths)
+        _lib.call("cs_init_fcc", nu, aa, LL, float(jitter), int(seed), _lib.ptr(b["x"]),
+                  _lib.ptr(b["y"]), _lib.ptr(b["z"]), _lib.ptr(b["id"]), self._s())
+        _lib.call("cs_init_velocities", self.n, float(temperature), self.params.mass, int(seed),
+                  _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]), _lib.ptr(self._ws),
+                  self._wsb, self._s())
+        self.initial = {k: b[k].clone() for k in ("x", "y", "z", "vx", "vy", "vz", "id")}
+        self.rebuild()
+
+    def load_host(self, x, y, z, vx, vy, vz, ids):
+        """Copy host arrays in (any order), rebuild cells and forces."""
+        torch = _torch()
+        b = self._buf[self.cur]
+        for k, arr in zip(("x", "y", "z", "vx", "vy", "vz"), (x, y, z, vx, vy, vz)):
+            b[k][: self.n].copy_(torch.as_tensor(arr, dtype=torch.float64))
+        b["id"][: self.n].copy_(torch.as_tensor(ids, dtype=torch.int32))
+        self.rebuild()
+
+    def rebuild(self, energy: bool = True):
+        self.build_cells()
+        self.compute_forces(energy=energy)
+
+    # ------------------------------------------------------------- kernels
+    def build_cells(self):
+        """K1: stable counting sort into the other buffer, then swap."""
+        a, b = self._buf[self.cur], self._buf[1 - self.cur]
+        _lib.call("cs_build_cells", self.n, C.byref(self._cbox), _lib.ptr(a["x"]), _lib.ptr(a["y"]),
+                  _lib.ptr(a["z"]), _lib.ptr(a["vx"]), _lib.ptr(a["vy"]), _lib.ptr(a["vz"]),
+                  _lib.ptr(a["id"]), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]),
+                  _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]), _lib.ptr(b["id"]),
+                  _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), _lib.ptr(self.cell_start),
+                  _lib.ptr(self._ws), self._wsb, self._s())
+        self.cur = 1 - self.cur
+
+    def compute_forces(self, energy: bool = False, count_pairs: bool = True):
+        """K2 (forces must be zero on entry; build_cells zeroes them)."""
+        b = self._buf[self.cur]
+        if energy:
+            self.scal[0:1].zero_()
+        if count_pairs:
+            self.npairs.zero_()
+        _lib.call("cs_lj_forces", C.byref(self._cbox), C.byref(self._clj), SCHEDULES[self.schedule],
+                  _lib.ptr(self.cell_start), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]),
+                  _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]),
+                  _lib.ptr(self.scal) if energy else None,
+                  _lib.ptr(self.npairs) if count_pairs else None,
+                  _lib.ptr(self._ws), self._wsb, self._s())
+
+    def kinetic(self):
+        b = self._buf[self.cur]
+        _lib.call("cs_kinetic", self.n, self.params.mass, _lib.ptr(b["vx"]), _lib.ptr(b["vy"]),
+                  _lib.ptr(b["vz"]), _lib.ptr(self.scal[1:]), _lib.ptr(self._ws), self._wsb, self._s())
+
+    def step(self, energy: bool = False):
+        """One velocity-Verlet step (K3 kick+drift, K1, K2, K3 kick)."""
+        hdtm = 0.5 * self.dt / self.params.mass
+        b = self._buf[self.cur]
+        _lib.call("cs_vv_kick_drift", self.n, hdtm, self.dt, C.byref(self._cbox), _lib.ptr(b["fx"]),
+                  _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), _lib.ptr(b["vx"]), _lib.ptr(b["vy"]),
+                  _lib.ptr(b["vz"]), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]), self._s())
+        self.build_cells()
+        self.compute_forces(energy=energy)
+        b = self._buf[self.cur]
+        _lib.call("cs_vv_kick", self.n, hdtm, _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]),
+                  _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]), self._s())
+        if energy:
+            self.kinetic()
+
+    # ---------------------------------------------------------- CUDA graph
+    def graph_step(self, energy: bool = False):
+        """Replay one step from a captured CUDA graph (two graphs: one per
+        ping-pong parity, since each step swaps the buffers)."""
+        torch = _torch()
+        key = (self.cur, energy)
+        if key not in self._graphs:
+            start = self.cur
+            s = torch.cuda.Stream(device=self.device)
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                saved = [t.clone() for t in self._state_tensors()]
+                self.step(energy)  # warm-up outside capture
+                torch.cuda.synchronize()
+                self.cur = start
+                with torch.cuda.graph(g, stream=s):
+                    self.step(energy)
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            # restore the pre-warm-up state: capture must not advance time
+            for t, v in zip(self._state_tensors(), saved):
+                t.copy_(v)
+            self.cur = start
+            self._graphs[key] = g
+        self._graphs[key].replay()
+        self.cur = 1 - self.cur
+
+    def _state_tensors(self):
+        out = []
+        for b in self._buf:
+            out += [b[k] for k in ("x", "y", "z", "vx", "vy", "vz", "fx", "fy", "fz", "id")]
+        return out + [self.cell_start, self.scal, self.npairs]
+
+    def run(self, nsteps: int, energy_every: int = 0, graph: bool = True):
+        """Advance nsteps; returns [(step, pe, ke)] at the energy steps."""
+        out = []
+        for k in range(1, nsteps + 1):
+            en = energy_every > 0 and k % energy_every == 0
+            (self.graph_step if graph else self.step)(energy=en)
+            if en:
+                pe, ke = self.energies()
+                out.append((k, pe, ke))
+        return out
+
+    # -------------------------------------------------------------- output
+    def energies(self):
+        """(PE, KE) of the last energy evaluation (synchronises)."""
+        v = self.scal.cpu().tolist()
+        return v[0], v[1]
+
+    def pair_count(self) -> int:
+        return int(self.npairs.item())
+
+    def snapshot(self):
+        """Host copies in cell-sorted order: x, v, f as (n, 3), ids, cell_start."""
+        torch = _torch()
+        b = self._buf[self.cur]
+        n = self.n
+        st = lambda ks: torch.stack([b[k][:n] for k in ks], 1).cpu().numpy()
+        return {"x": st(("x", "y", "z")), "v": st(("vx", "vy", "vz")), "f": st(("fx", "fy", "fz")),
+                "id": b["id"][:n].cpu().numpy(), "cell_start": self.cell_start.cpu().numpy()}
+
+
+# reference-style functional entry points ------------------------------------
+def build_cell_list(system: LJSystem) -> None:
+    system.build_cells()
+
+
+def lj_forces(system: LJSystem, energy: bool = True):
+    """Zero the forces, evaluate them; returns (PE, pairs within rc)."""
+    for k in ("fx", "fy", "fz"):
+        system._a(k).zero_()
+    system.compute_forces(energy=energy)
+    return system.energies()[0], system.pair_count()
+
+
+def vv_step(system: LJSystem, energy: bool = False) -> None:
+    system.step(energy=energy)
