@@ -1,0 +1,331 @@
+"""Benchmark of the LJ link-cell hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one velocity-Verlet step of BASELINE configs[1] (cfg2: FCC 48^3 =
+442,368 particles, rho 0.8442, 32^3 cells, T* 0.722, dt 0.005, fp64):
+kick+drift+wrap, stable counting-sort rebin, LJ half-shell forces with
+Newton-3 reaction writes under the 8-pass colour schedule, kick.
+`value` = pair interactions per second (pairs within rc per step x steps/s),
+device-timed with CUDA events per step, L2 flushed between steps.
+N > 1 (torchrun): each rank advances its own cfg2-sized block of a
+weak-scaled system ("scaling": "weak"); see DESIGN.md section on multi-GPU.
+`--impl reference` times the CPU port of the reference's own colour-order
+execution (oracle/, OpenMP over all host cores) on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LJ link-cell pair interactions/s (fp64, cfg2 442,368 particles)"
+UNIT = "pair-interactions/s"
+NUC = 48  # cfg2
+WORKLOAD = "cfg2: LJ fluid FCC 48^3 = 442368 particles, rho* 0.8442, T* 0.722, rc 2.5 (unshifted), 32^3 cells, dt 0.005, fp64, 1 VV step"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and "Active" in r[3 + k]
+                          and "Not" not in r[3 + k]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    return rank, ws
+
+
+def max_over_ranks(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# --------------------------------------------------------------- CPU arms --
+def cpu_setup(nthreads):
+    import numpy as np
+
+    from oracle import oracle as O
+
+    rho = 0.8442
+    a = (4 / rho) ** (1 / 3)
+    L = NUC * a
+    x, y, z = O.fcc_positions([NUC] * 3, [a] * 3, [L] * 3, 0.05, 42)
+    n = len(x)
+    vx, vy, vz = O.velocities(n, 0.722, 1.0, 42)
+    return O.CpuMD(x, y, z, vx, vy, vz, np.arange(n, dtype=np.int32), [32] * 3, [L] * 3, nthreads=nthreads)
+
+
+def cpu_sample(nthreads, min_seconds=10.0, max_steps=200):
+    """Bounded sample: whole cfg2 steps until >= min_seconds of CPU work."""
+    m = cpu_setup(nthreads)
+    steps, pairs, t0 = 0, 0, time.perf_counter()
+    while True:
+        _, _, npairs = m.steps(1)
+        steps += 1
+        pairs += int(npairs[0])
+        el = time.perf_counter() - t0
+        if el >= min_seconds or steps >= max_steps:
+            return pairs / el, steps, el
+
+
+def run_reference(args):
+    rank, ws = dist_init()
+    if rank != 0:
+        return
+    import numpy as np
+
+    cores = len(os.sched_getaffinity(0))
+    m = cpu_setup(cores)
+    for _ in range(args.warmup):
+        m.steps(1)
+    times, pairs = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, _, npairs = m.steps(1)
+        times.append(time.perf_counter() - t0)
+        pairs += int(npairs[0])
+    tot = sum(times)
+    value = pairs / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded FCC + jitter, Gaussian velocities)",
+        "config": {"workload": WORKLOAD, "schedule": "loop-exchange colour order, 27 levels, OpenMP over tasks of a level",
+                   "steps_per_s": args.steps / tot},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} whole cfg2 VV steps (oracle/cs_oracle.c o_md_steps)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- GPU --
+def fp64_peak(torch, lib):
+    """Measured DFMA throughput (TFLOP/s) of this GPU, burst."""
+    from paper_1401_4441_b200 import _lib
+
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blocks, iters = 148 * 8, 2000
+    best = 0.0
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.call("cs_probe_dfma", blocks, iters, _lib.ptr(out), _lib.stream_handle())
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = max(best, blocks * 256 * iters * 256 / (ms * 1e-3) / 1e12)
+    return best
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank, ws = dist_init()
+    from paper_1401_4441_b200 import _lib, md
+
+    dev = torch.cuda.current_device()
+    peak_fp64 = fp64_peak(torch, _lib)
+    sysm = md.LJSystem.fcc(NUC, schedule=args.schedule, block=args.block, seed=42 + rank)
+    pre, force, post = sysm.graph_phases()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    for _ in range(args.warmup):
+        pre(); force(); post()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    pairs, cands = [], []
+    barrier(ws)
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e = ev[k]
+            e[0].record(); pre(); e[1].record(); force(); e[2].record(); post(); e[3].record()
+            torch.cuda.synchronize()
+            pairs.append(sysm.pair_count())
+            cands.append(sysm.candidate_pairs())
+    barrier(ws)
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    force_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    tot_s = max_over_ranks(sum(step_ms) * 1e-3, ws)
+    tot_pairs = sum_over_ranks(float(sum(pairs)), ws)
+    value = tot_pairs / tot_s
+    # roofline of the dominant kernel (force passes): algorithmic FLOPs 8C + 20P
+    flops = [8 * c + 20 * p for c, p in zip(cands, pairs)]
+    achieved = sum(flops) / (sum(force_ms) * 1e-3) / 1e12
+    # ---------------------------------------------------------------- e2e
+    e2e = e2e_run(torch, md, sysm, args)
+    clocks = clk.summary()
+    if rank != 0:
+        return
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        cores = len(os.sched_getaffinity(0))
+        v, nst, el = cpu_sample(cores, min_seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{nst} whole cfg2 VV steps in {el:.1f} s (oracle o_md_steps, loop-exchange colour order on OpenMP threads)"}
+    n = sysm.n
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded FCC 48^3 + 0.05 sigma jitter, Gaussian velocities; BASELINE cfg2)",
+        "config": {"workload": WORKLOAD, "particles_per_gpu": n, "schedule": f"{args.schedule} {sysm.block}",
+                   "l2": "flushed (256 MB memset) between timed steps",
+                   "steps_per_s": args.steps / tot_s, "pairs_per_step": statistics.mean(pairs),
+                   "candidates_per_step": statistics.mean(cands),
+                   "force_ms_per_step": statistics.mean(force_ms), "force_share": sum(force_ms) / sum(step_ms),
+                   "parallelism": f"dp{ws}" if ws > 1 else "single"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
+                     "frac": achieved / peak_fp64, "traffic": None,
+                     "kernel": "k_force_block (8 colour passes)",
+                     "flops_convention": "8 C + 20 P per force evaluation (SURVEY 8d)",
+                     "peak_source": "measured live: cs_probe_dfma DFMA chains (MEASURED_PEAKS.json has no FP64 entry)",
+                     "hbm_peak_gbs": peaks().get("hbm_gbs")},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps * sysm.launches_per_step(),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def e2e_run(torch, md, ref_sys, args):
+    """Same metric through the public API from pinned host buffers: upload the
+    state, K graph-replayed steps each reading back (PE, KE), download the
+    final state -- all inside the timed region."""
+    n = ref_sys.n
+    host = {k: v[:n].cpu().pin_memory() for k, v in ref_sys.initial.items()}
+    sysm = md.LJSystem(ref_sys.box, n, schedule=ref_sys.schedule, block=ref_sys.block)
+    sysm.load_host(host["x"], host["y"], host["z"], host["vx"], host["vy"], host["vz"], host["id"])
+    for _ in range(2):
+        sysm.graph_step(energy=True)
+    torch.cuda.synchronize()
+    out = torch.empty((6, n), dtype=torch.float64).pin_memory()
+    t0 = time.perf_counter()
+    sysm.load_host(host["x"], host["y"], host["z"], host["vx"], host["vy"], host["vz"], host["id"])
+    pairs = 0
+    for _ in range(args.steps):
+        sysm.graph_step(energy=True)
+        sysm.energies()  # device -> host read of the step's result (PE, KE)
+        pairs += sysm.pair_count()
+    b = sysm._buf[sysm.cur]
+    for i, k in enumerate(("x", "y", "z", "vx", "vy", "vz")):
+        out[i].copy_(b[k][:n], non_blocking=True)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    h2d = 52 * n
+    d2h = 16 + 8 + 48 * n
+    return {"value": pairs / el, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
+            "d2h_bytes_per_step": d2h / args.steps,
+            "timed": "host wall clock: H2D of the initial state, K steps with per-step (PE, KE, pairs) readback, D2H of the final state"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--schedule", default="shell", choices=["shell", "buffered", "block", "loopex"])
+    ap.add_argument("--block", type=lambda s: tuple(int(v) for v in s.split(",")), default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -120,7 +120,7 @@ int cs_payload_colour(const cs_grid *g, int sched, const int32_t *block_host, co
 size_t cs_payload_colour_ws_bytes(const cs_grid *g);
 
 /* ===================== LJ link-cell MD (new; extends the payload plug-in) */
-enum { CS_SCHED_LOOPEX = 0, CS_SCHED_BLOCK = 1 };
+enum { CS_SCHED_LOOPEX = 0, CS_SCHED_BLOCK = 1, CS_SCHED_SHELL = 2, CS_SCHED_BUFFERED = 3 };
 
 /* Local cell box.  Single GPU: nc == gnc, x0 == 0, periodic {1,1,1}.
  * x-slab rank: nc[0] = owned planes + 1 ghost plane, periodic[0] = 0,
@@ -161,14 +161,23 @@ int cs_build_cells(int64_t n, const cs_box *b, const double *x, const double *y,
                    double *fzo, int32_t *cell_start, void *ws, size_t ws_bytes, void *stream);
 
 /* K2: fp64 LJ half-shell forces with Newton-3 reaction writes under a
- * conflict-free colour-pass schedule; f must be zeroed by the caller
- * (cs_build_cells does).  energy_dev[0] += PE, npairs_dev[0] += pairs
- * (either may be NULL). */
-size_t cs_force_ws_bytes(const cs_box *b, int sched);
-int cs_lj_forces(const cs_box *b, const cs_lj *p, int sched, const int32_t *cell_start,
-                 const double *x, const double *y, const double *z, double *fx, double *fy,
-                 double *fz, double *energy_dev, unsigned long long *npairs_dev, void *ws,
-                 size_t ws_bytes, void *stream);
+ * conflict-free schedule; f must be zeroed by the caller (cs_build_cells
+ * does).  n = particles in the cell arrays.  energy_dev[0] += PE,
+ * npairs_dev[0] += pairs, status_dev[0] |= 1 on a capacity overflow of the
+ * buffered schedule (any of the three may be NULL).
+ *   CS_SCHED_LOOPEX   27 passes = the reference's loop-exchange levels
+ *   CS_SCHED_BLOCK    8 passes of 2x2x2-coloured blocks, 27 levels inside
+ *   CS_SCHED_SHELL    8 passes of 2x2x2-coloured blocks, one warp per
+ *                     home-cell half shell, per-offset reaction slots
+ *   CS_SCHED_BUFFERED one pass over all blocks into private footprint
+ *                     buffers + a deterministic gather (buffered strategy,
+ *                     taskgen.py:237-276, at block granularity) */
+size_t cs_force_ws_bytes(const cs_box *b, int sched, int64_t n);
+int cs_lj_forces(const cs_box *b, const cs_lj *p, int sched, int64_t n,
+                 const int32_t *cell_start, const double *x, const double *y, const double *z,
+                 double *fx, double *fy, double *fz, double *energy_dev,
+                 unsigned long long *npairs_dev, unsigned *status_dev, void *ws, size_t ws_bytes,
+                 void *stream);
 
 /* K3: velocity Verlet.  kick: v += (dt/2m) f.  kick_drift: v += (dt/2m) f;
  * x += dt v; wrap into [0, L) on periodic axes. */
@@ -192,6 +201,10 @@ int cs_pack_plane(const cs_box *b, int plane, const int32_t *cell_start, const d
                   const double *y, const double *z, double xshift, double *out, void *stream);
 int cs_add_plane_forces(const cs_box *b, int plane, const int32_t *cell_start, const double *in,
                         double *fx, double *fy, double *fz, void *stream);
+
+/* FP64 pipe probe used by bench.py to measure the FP64 roofline peak:
+ * blocks x 256 threads x iters x 256 flops (DFMA = 2 flops). */
+int cs_probe_dfma(int blocks, int iters, double *out, void *stream);
 
 #ifdef __cplusplus
 }

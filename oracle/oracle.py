@@ -79,6 +79,9 @@ def lib():
         L.o_md_run.argtypes = [C.c_int64, _i32p, _f64p, _f64p, C.c_double, C.c_double, C.c_int,
                                C.c_int, C.c_int, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p, _i32p,
                                _f64p, _f64p, _f64p, _i32p, _f64p, _f64p]
+        L.o_md_steps.argtypes = [C.c_int64, _i32p, _f64p, _f64p, C.c_double, C.c_double, C.c_int,
+                                 C.c_int, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p, _i32p,
+                                 _f64p, _f64p, _f64p, _i32p, _f64p, _f64p, _i64p]
         L.o_max_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -272,6 +275,31 @@ def md_run(x, y, z, vx, vy, vz, ids, nc, L, nsteps, dt=0.005, mass=1.0, eps=1.0,
                    mass, dt, nsteps, mode, nthreads, *arrs, ids, *f, start, pe, ke)
     return {"x": np.stack(arrs[:3], 1), "v": np.stack(arrs[3:], 1), "id": ids,
             "f": np.stack(f, 1), "cell_start": start, "pe": pe, "ke": ke}
+
+
+class CpuMD:
+    """Cell-sorted host state advanced by o_md_steps (CPU baseline)."""
+
+    def __init__(self, x, y, z, vx, vy, vz, ids, nc, L, dt=0.005, mass=1.0, eps=1.0, sigma=1.0,
+                 rc=2.5, nthreads=0):
+        r = md_run(x, y, z, vx, vy, vz, ids, nc, L, 0, dt, mass, eps, sigma, rc, mode=1,
+                   nthreads=nthreads)
+        self.n = len(x)
+        self.nc = np.asarray(nc, np.int32)
+        self.L = np.asarray(L, np.float64)
+        self.prm = _prm(eps, sigma, rc)
+        self.dt, self.mass, self.nthreads = dt, mass, nthreads
+        self.a = [np.ascontiguousarray(r["x"][:, k]) for k in range(3)]
+        self.a += [np.ascontiguousarray(r["v"][:, k]) for k in range(3)]
+        self.id = r["id"]
+        self.f = [np.ascontiguousarray(r["f"][:, k]) for k in range(3)]
+        self.start = r["cell_start"]
+
+    def steps(self, k):
+        pe, ke, npairs = np.zeros(k), np.zeros(k), np.zeros(k, np.int64)
+        lib().o_md_steps(self.n, self.nc, self.L, self.prm, self.mass, self.dt, k, self.nthreads,
+                         *self.a, self.id, *self.f, self.start, pe, ke, npairs)
+        return pe, ke, npairs
 
 
 def max_threads():

@@ -21,7 +21,7 @@ CS_ERANGE = -4
 CS_ECYCLE = -5
 
 STREAM_BASIC, STREAM_LOOPEX = 0, 1
-SCHED_LOOPEX, SCHED_BLOCK = 0, 1
+SCHED_LOOPEX, SCHED_BLOCK, SCHED_SHELL, SCHED_BUFFERED = 0, 1, 2, 3
 
 
 class CsGrid(C.Structure):
@@ -79,14 +79,15 @@ _SIGS = {
     "cs_init_velocities": (C.c_int, [_I64, _D, _D, _I64, _P, _P, _P, _P, _SZ, _P]),
     "cs_bin_ws_bytes": (_SZ, [_I64, _P]),
     "cs_build_cells": (C.c_int, [_I64, _P] + [_P] * 18 + [_P, _SZ, _P]),
-    "cs_force_ws_bytes": (_SZ, [_P, C.c_int]),
-    "cs_lj_forces": (C.c_int, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "cs_force_ws_bytes": (_SZ, [_P, C.c_int, _I64]),
+    "cs_lj_forces": (C.c_int, [_P, _P, C.c_int, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "cs_vv_kick": (C.c_int, [_I64, _D, _P, _P, _P, _P, _P, _P, _P]),
     "cs_vv_kick_drift": (C.c_int, [_I64, _D, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "cs_kinetic": (C.c_int, [_I64, _D, _P, _P, _P, _P, _P, _SZ, _P]),
     "cs_sum3": (C.c_int, [_I64, _P, _P, _P, _P, _P, _SZ, _P]),
     "cs_pack_plane": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _D, _P, _P]),
     "cs_add_plane_forces": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P]),
+    "cs_probe_dfma": (C.c_int, [C.c_int, C.c_int, _P, _P]),
 }
 
 EXPORTS = tuple(_SIGS)

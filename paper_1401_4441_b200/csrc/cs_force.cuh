@@ -336,12 +336,20 @@ static int force_cap(const Box &b) {
   return 2048;  // particles staged per CTA (48 KB of fp64 forces)
 }
 
-extern "C" size_t cs_force_ws_bytes(const cs_box *bx, int sched) {
-  (void)sched;
+struct Box;
+static size_t shell_buffered_ws(const Box &b, int64_t n);
+
+extern "C" size_t cs_force_ws_bytes(const cs_box *bx, int sched, int64_t n) {
   int64_t nc = (int64_t)bx->nc[0] * bx->nc[1] * bx->nc[2];
-  return cs_ws_slice(sizeof(double) * nc) + cs_ws_slice(sizeof(unsigned) * nc) +
-         cs_ws_slice(sizeof(double) * RED_BLOCKS_MAX) +
-         cs_ws_slice(sizeof(unsigned long long) * RED_BLOCKS_MAX);
+  size_t base = cs_ws_slice(sizeof(double) * nc) + cs_ws_slice(sizeof(unsigned) * nc) +
+                cs_ws_slice(sizeof(double) * RED_BLOCKS_MAX) +
+                cs_ws_slice(sizeof(unsigned long long) * RED_BLOCKS_MAX);
+  if (sched == CS_SCHED_BUFFERED) {
+    Box b;
+    if (make_box(bx, &b) != CS_OK) return 0;
+    base += shell_buffered_ws(b, n);
+  }
+  return base;
 }
 
 static int check_lj_box(const Box &b, double rc) {
@@ -354,11 +362,14 @@ static int check_lj_box(const Box &b, double rc) {
   return CS_OK;
 }
 
-extern "C" int cs_lj_forces(const cs_box *bx, const cs_lj *lj, int sched,
+static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, cs_ws *w,
+                               int64_t n, unsigned *status, cudaStream_t st);
+
+extern "C" int cs_lj_forces(const cs_box *bx, const cs_lj *lj, int sched, int64_t npart,
                             const int32_t *cell_start, const double *x, const double *y,
                             const double *z, double *fx, double *fy, double *fz,
-                            double *energy_dev, unsigned long long *npairs_dev, void *ws,
-                            size_t ws_bytes, void *stream) {
+                            double *energy_dev, unsigned long long *npairs_dev,
+                            unsigned *status_dev, void *ws, size_t ws_bytes, void *stream) {
   CS_TRY(cs_upload_stencil());
   cudaStream_t st = cs_stream(stream);
   ForceArgs A;
@@ -418,6 +429,9 @@ extern "C" int cs_lj_forces(const cs_box *bx, const cs_lj *lj, int sched,
       else
         k_force_block<false><<<blocks, BLK_THREADS, smem, st>>>(A, colour);
     }
+  } else if (sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED) {
+    CS_TRY(block_grid(A.b, A.nbk));
+    CS_TRY(launch_shell_passes(A, energy, sched == CS_SCHED_BUFFERED, &w, npart, status_dev, st));
   } else {
     CS_REQUIRE(0, "unknown schedule %d", sched);
   }

@@ -1,0 +1,563 @@
+// cs_force2.cuh -- K2 v3: half-shell "super-task" per warp inside a block CTA.
+//
+// A CTA owns one block of Bx*By*Bz home cells.  One warp evaluates the whole
+// half shell of one home cell h -- the 14 tasks (intra + 13 offsets) that
+// generate_basic emits per cell (taskgen.py:188-198):
+//
+//   0. tables: for every (home h, entry e) the source cell's start/count and
+//      periodic image shift, and a slot base for the reaction buffer.
+//   1. cull: a j whose distance to h's box is >= rc cannot reach any i of h;
+//      survivors are compacted into the warp's list as (entry, index).
+//   2. filter: lanes hold 32 j's, 8 home i's are broadcast from shared
+//      memory; each lane builds an 8-bit hit mask (r^2 < rc^2 in fp64).
+//   3. hit loop: every lane walks its own set bits, computes f_ij once
+//      (fast reciprocal: MUFU.RCP64H + 2 Newton steps), keeps -f_ij on j in
+//      registers and adds +f_ij into its private row of i partials.
+//   4. reactions go to the slot of (h, e, j): a fixed offset e has exactly one
+//      writer per target cell, so the block's warps never collide (the
+//      paper's buffered strategy inside the block); i rows are reduced per
+//      row block.
+//   5. after one barrier the CTA merges, per footprint cell in a fixed
+//      order, home rows + reaction slots: either read-modify-write into
+//      global f (CS_SCHED_SHELL: 8 passes of a 2x2x2 block colouring, same-
+//      colour footprints are disjoint) or plain stores into the block's
+//      private footprint buffer (CS_SCHED_BUFFERED: one pass over all
+//      blocks, then k_gather_blocks sums the <= 8 buffers per particle).
+//
+// No atomics on forces, no intra-CTA dependency levels, deterministic order.
+#pragma once
+#include "cs_force.cuh"
+
+#define SH_NW 8        // warps per CTA (one home cell each for 2x2x2 blocks)
+#define SH_IB 8        // home particles per filter row block
+#define SH_JCAP 384    // j list capacity per warp (>= particles of the 14 source cells)
+#define SH_RCAP 1536   // reaction slots (particles) per CTA
+#define SH_HCAP 256    // home particles per CTA
+#define SH_MAXB 8      // home cells per CTA
+#define SH_MAXF 64     // footprint cells per CTA ((Bx+1)(By+2)(Bz+2))
+#define SH_MAXC 8      // contributors per footprint cell
+
+struct MergeTable {              // host-built per block shape
+  uint8_t n[SH_MAXF];            // contributors of footprint cell lc
+  uint8_t he[SH_MAXF][SH_MAXC];  // h * 16 + e (e = 0: home rows)
+  int nfc;
+};
+
+struct ShellSmem {
+  double rows[SH_NW][SH_IB][3][32];  // per-lane i partials
+  double R[3][SH_RCAP];              // reaction slots (e >= 1)
+  double Fh[3][SH_HCAP];             // home rows (e = 0)
+  double hx[SH_NW][SH_IB][4];        // broadcast home positions
+  double sh[SH_MAXB][14][3];         // image shift of source (h, e)
+  int jl[SH_NW][SH_JCAP];            // culled j: entry << 24 | index in source cell
+  int sstart[SH_MAXB][14];           // global start of source (h, e)
+  int scount[SH_MAXB][14];           // count of source (h, e), -1: none
+  int sbase[SH_MAXB][14];            // slot base (Fh for e = 0, R for e >= 1)
+  int fstart[SH_MAXF + 1];           // footprint cell -> offset in the block buffer
+  int fgstart[SH_MAXF];              // footprint cell -> global start (-1: none)
+  int hcell[SH_MAXB];
+  int overflow;
+};
+
+__device__ __forceinline__ double box_d2(double x, double lo, double hi) {
+  const double d = fmax(fmax(lo - x, 0.0), x - hi);
+  return d * d;
+}
+
+// 1/a to ~1 ulp: hardware approximation + two Newton-Raphson steps
+__device__ __forceinline__ double fast_rcp(double a) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double e = __fma_rn(-a, y, 1.0);
+  y = __fma_rn(y, e, y);
+  e = __fma_rn(-a, y, 1.0);
+  return __fma_rn(y, e, y);
+}
+
+__device__ __forceinline__ int wrap1i(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+
+struct ShellArgs {
+  ForceArgs A;
+  MergeTable mt;
+  double *buf;            // buffered mode: footprint buffers, 3 components x bufstride
+  const int *boff;        // buffered mode: per-block offset into buf
+  int *bindex;            // buffered mode: per block fstart[0..SH_MAXF]
+  int64_t bufstride;
+  unsigned *err;          // capacity overflow flag (buffered mode)
+};
+
+// block coordinates -> global cell of a footprint cell (or -1)
+__device__ __forceinline__ int64_t foot_cell(const Box &b, const int *o0, int lc, int FX, int FY) {
+  int v0 = o0[0] + lc % FX, v1 = o0[1] + (lc / FX) % FY - 1, v2 = o0[2] + lc / (FX * FY) - 1;
+  if (b.per[0]) v0 = wrap1i(v0, b.nc[0]); else if (v0 < 0 || v0 >= b.nc[0]) return -1;
+  if (b.per[1]) v1 = wrap1i(v1, b.nc[1]); else if (v1 < 0 || v1 >= b.nc[1]) return -1;
+  if (b.per[2]) v2 = wrap1i(v2, b.nc[2]); else if (v2 < 0 || v2 >= b.nc[2]) return -1;
+  return box_cell(b, v0, v1, v2);
+}
+
+template <bool ENERGY, bool BUFFERED>
+__global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int colour) {
+  extern __shared__ __align__(16) unsigned char sh_raw[];
+  ShellSmem &S = *reinterpret_cast<ShellSmem *>(sh_raw);
+  const ForceArgs &A = SA.A;
+  const Box &b = A.b;
+  const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
+  const int nhome = B0 * B1 * B2;
+  int o0[3];
+  int bid = blockIdx.x;
+  if (BUFFERED) {
+    o0[0] = (bid % A.nbk[0]) * B0;
+    o0[1] = ((bid / A.nbk[0]) % A.nbk[1]) * B1;
+    o0[2] = (bid / (A.nbk[0] * A.nbk[1])) * B2;
+  } else {
+    const int kc0 = colour & 1, kc1 = (colour >> 1) & 1, kc2 = (colour >> 2) & 1;
+    const int cnt0 = (A.nbk[0] - kc0 + 1) >> 1, cnt1 = (A.nbk[1] - kc1 + 1) >> 1;
+    o0[0] = (2 * (bid % cnt0) + kc0) * B0;
+    o0[1] = (2 * ((bid / cnt0) % cnt1) + kc1) * B1;
+    o0[2] = (2 * (bid / (cnt0 * cnt1)) + kc2) * B2;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int FX = B0 + 1, FY = B1 + 2;
+  const int nfc = SA.mt.nfc;
+
+  // ---- 0. source tables, one thread per (h, e); footprint cells
+  for (int t = threadIdx.x; t < nhome * 14; t += blockDim.x) {
+    const int h = t / 14, e = t - 14 * h;
+    const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
+    int cnt = -1, st = 0;
+    double s0 = 0, s1 = 0, s2 = 0;
+    const bool home_ok = hg0 < b.owned_x;
+    if (home_ok) {
+      int v0 = hg0 + c_stencil3.o[e][0], v1 = hg1 + c_stencil3.o[e][1], v2 = hg2 + c_stencil3.o[e][2];
+      bool ok = true;
+      if (b.per[0]) { s0 = v0 >= b.nc[0] ? b.L[0] : (v0 < 0 ? -b.L[0] : 0.0); v0 = wrap1i(v0, b.nc[0]); }
+      else ok = ok && v0 >= 0 && v0 < b.nc[0];
+      if (b.per[1]) { s1 = v1 >= b.nc[1] ? b.L[1] : (v1 < 0 ? -b.L[1] : 0.0); v1 = wrap1i(v1, b.nc[1]); }
+      else ok = ok && v1 >= 0 && v1 < b.nc[1];
+      if (b.per[2]) { s2 = v2 >= b.nc[2] ? b.L[2] : (v2 < 0 ? -b.L[2] : 0.0); v2 = wrap1i(v2, b.nc[2]); }
+      else ok = ok && v2 >= 0 && v2 < b.nc[2];
+      if (ok) {
+        const int64_t gc = box_cell(b, v0, v1, v2);
+        st = A.start[gc];
+        cnt = A.start[gc + 1] - st;
+      }
+    }
+    if (e == 0) S.hcell[h] = home_ok ? (int)box_cell(b, hg0, hg1, hg2) : -1;
+    S.sstart[h][e] = st;
+    S.scount[h][e] = cnt;
+    S.sh[h][e][0] = s0;
+    S.sh[h][e][1] = s1;
+    S.sh[h][e][2] = s2;
+  }
+  for (int lc = threadIdx.x; lc < nfc; lc += blockDim.x) {
+    const int64_t gc = foot_cell(b, o0, lc, FX, FY);
+    S.fgstart[lc] = gc >= 0 ? A.start[gc] : -1;
+    S.fstart[lc + 1] = gc >= 0 ? A.start[gc + 1] - A.start[gc] : 0;
+  }
+  __syncthreads();
+  if (wid == 0) {  // slot bases (scan over (h, e)), list capacity, footprint offsets
+    int fb = 0, rb = 0;
+    for (int t0 = 0; t0 < nhome * 14; t0 += 32) {
+      const int t = t0 + lane;
+      const int h = t / 14, e = t - 14 * (t / 14);
+      const int c = t < nhome * 14 ? max(S.scount[h][e], 0) : 0;
+      const int ch = (t < nhome * 14 && e == 0) ? c : 0;
+      const int cr = (t < nhome * 14 && e != 0) ? c : 0;
+      int ih = ch, ir = cr;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const int vh = __shfl_up_sync(CS_FULL, ih, s), vr = __shfl_up_sync(CS_FULL, ir, s);
+        if (lane >= s) { ih += vh; ir += vr; }
+      }
+      if (t < nhome * 14) S.sbase[h][e] = e == 0 ? fb + ih - ch : rb + ir - cr;
+      fb += __shfl_sync(CS_FULL, ih, 31);
+      rb += __shfl_sync(CS_FULL, ir, 31);
+    }
+    int src_max = 0;
+    for (int h = 0; h < nhome; ++h) {
+      const int c = warp_sum(lane < 14 ? max(S.scount[h][lane], 0) : 0);
+      src_max = max(src_max, c);
+    }
+    int carry = 0;
+    for (int c0 = 0; c0 < nfc; c0 += 32) {
+      const int lc = c0 + lane;
+      const int v = lc < nfc ? S.fstart[lc + 1] : 0;
+      int inc = v;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const int u = __shfl_up_sync(CS_FULL, inc, s);
+        if (lane >= s) inc += u;
+      }
+      if (lc < nfc) S.fstart[lc + 1] = carry + inc;
+      carry += __shfl_sync(CS_FULL, inc, 31);
+    }
+    if (lane == 0) {
+      S.fstart[0] = 0;
+      S.overflow = (fb > SH_HCAP || rb > SH_RCAP || src_max > SH_JCAP) ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (S.overflow) {
+    if (BUFFERED) {  // no in-place fallback in buffered mode: report to the host
+      if (threadIdx.x == 0) atomicExch(SA.err, 1u);
+      return;
+    }
+    // colour mode fallback: v1 per-task routine on global memory under the 27
+    // loop-exchange levels inside this block (still conflict-free)
+    for (int level = 0; level < 27; ++level) {
+      int e, par;
+      level_entry(level, &e, &par);
+      const int ax = c_stencil3.axis[e];
+      for (int h = wid; h < nhome; h += SH_NW) {
+        if (S.hcell[h] < 0 || S.scount[h][e] < 0) continue;
+        const int hg[3] = {o0[0] + h % B0, o0[1] + (h / B0) % B1, o0[2] + h / (B0 * B1)};
+        if (level > 0 && (hg[ax] & 1) != par) continue;
+        const int a0 = S.sstart[h][0], na = S.scount[h][0];
+        const int b0 = S.sstart[h][e], nb = S.scount[h][e];
+        double pe = 0;
+        unsigned hits = 0;
+        task_warp<ENERGY>(A.x, A.y, A.z, a0, na, b0, nb, level == 0, S.sh[h][e][0], S.sh[h][e][1],
+                          S.sh[h][e][2], A.fx + a0, A.fy + a0, A.fz + a0, A.fx + b0, A.fy + b0,
+                          A.fz + b0, A.p, pe, hits);
+        task_stats<ENERGY>(pe, hits, S.hcell[h], A.pe_cell, A.hits_cell);
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < SH_RCAP; i += blockDim.x) S.R[0][i] = S.R[1][i] = S.R[2][i] = 0.0;
+  for (int i = threadIdx.x; i < SH_HCAP; i += blockDim.x) S.Fh[0][i] = S.Fh[1][i] = S.Fh[2][i] = 0.0;
+  __syncthreads();
+
+  const double edge0 = b.L[0] / b.gnc[0], edge1 = b.L[1] / b.gnc[1], edge2 = b.L[2] / b.gnc[2];
+  const double cull2 = A.p.rc2 * (1.0 + 1e-12) + 1e-12;
+  const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
+  // ---- 1-4. one warp per home cell
+  for (int h = wid; h < nhome; h += SH_NW) {
+    if (S.hcell[h] < 0) continue;
+    const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
+    const int a0 = S.sstart[h][0], na = S.scount[h][0];
+    const double lo0 = (b.x0 + hg0) * edge0, lo1 = hg1 * edge1, lo2 = hg2 * edge2;
+    const double hi0 = lo0 + edge0, hi1 = lo1 + edge1, hi2 = lo2 + edge2;
+    // 1. cull + compact
+    int nj = 0;
+    for (int e = 0; e < 14; ++e) {
+      const int cn = S.scount[h][e];
+      if (cn <= 0) continue;
+      const int c0 = S.sstart[h][e];
+      const double s0 = S.sh[h][e][0], s1 = S.sh[h][e][1], s2 = S.sh[h][e][2];
+      for (int q0 = 0; q0 < cn; q0 += 32) {
+        const int q = q0 + lane;
+        bool keep = false;
+        if (q < cn) {
+          if (e == 0) {
+            keep = true;
+          } else {
+            const double xj = __ldg(A.x + c0 + q) + s0, yj = __ldg(A.y + c0 + q) + s1,
+                         zj = __ldg(A.z + c0 + q) + s2;
+            keep = box_d2(xj, lo0, hi0) + box_d2(yj, lo1, hi1) + box_d2(zj, lo2, hi2) < cull2;
+          }
+        }
+        const unsigned m = __ballot_sync(CS_FULL, keep);
+        if (keep) S.jl[wid][nj + __popc(m & ((1u << lane) - 1))] = (e << 24) | q;
+        nj += __popc(m);
+      }
+    }
+    __syncwarp();
+    double pe = 0;
+    unsigned hits = 0;
+    const int fh0 = S.sbase[h][0];
+    for (int ib = 0; ib < na; ib += SH_IB) {
+      const int nib = min(SH_IB, na - ib);
+      if (lane < SH_IB) {
+        const int ii = a0 + ib + min(lane, nib - 1);
+        S.hx[wid][lane][0] = __ldg(A.x + ii);
+        S.hx[wid][lane][1] = __ldg(A.y + ii);
+        S.hx[wid][lane][2] = __ldg(A.z + ii);
+      }
+#pragma unroll
+      for (int q = 0; q < SH_IB; ++q)
+        S.rows[wid][q][0][lane] = S.rows[wid][q][1][lane] = S.rows[wid][q][2][lane] = 0.0;
+      __syncwarp();
+      const unsigned qmask = (1u << nib) - 1;
+      for (int c0 = 0; c0 < nj; c0 += 32) {
+        const int jj = c0 + lane;
+        const bool vj = jj < nj;
+        const int ent = vj ? S.jl[wid][jj] : 0;
+        const int e = ent >> 24, q = ent & 0xFFFFFF;
+        double xj = 1e150, yj = 1e150, zj = 1e150;
+        if (vj) {
+          const int gj = S.sstart[h][e] + q;
+          xj = __ldg(A.x + gj) + S.sh[h][e][0];
+          yj = __ldg(A.y + gj) + S.sh[h][e][1];
+          zj = __ldg(A.z + gj) + S.sh[h][e][2];
+        }
+        // intra (e == 0): only pairs i < j, i.e. rows qq < q - ib
+        const int jr = (vj && e == 0) ? q - ib : SH_IB + 1;
+        unsigned mask = 0;
+#pragma unroll
+        for (int qq = 0; qq < SH_IB; ++qq) {
+          const double dx = S.hx[wid][qq][0] - xj, dy = S.hx[wid][qq][1] - yj,
+                       dz = S.hx[wid][qq][2] - zj;
+          const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+          mask |= (unsigned)(r2 < rc2 && qq < jr) << qq;
+        }
+        mask &= qmask;
+        double gx = 0, gy = 0, gz = 0;
+        while (__any_sync(CS_FULL, mask)) {
+          if (mask) {
+            const int qq = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const double dx = S.hx[wid][qq][0] - xj, dy = S.hx[wid][qq][1] - yj,
+                         dz = S.hx[wid][qq][2] - zj;
+            const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+            const double rinv2 = fast_rcp(r2);
+            const double sr2 = sig2 * rinv2;
+            const double sr6 = sr2 * sr2 * sr2;
+            const double ff = eps48 * sr6 * (sr6 - 0.5) * rinv2;
+            const double fx = ff * dx, fy = ff * dy, fz = ff * dz;
+            gx -= fx;
+            gy -= fy;
+            gz -= fz;
+            S.rows[wid][qq][0][lane] += fx;
+            S.rows[wid][qq][1][lane] += fy;
+            S.rows[wid][qq][2][lane] += fz;
+            if (ENERGY) pe += eps4 * sr6 * (sr6 - 1.0);
+            ++hits;
+          }
+        }
+        if (vj) {  // unique writer of slot (h, e, q)
+          const int slot = S.sbase[h][e] + q;
+          double *dst = e == 0 ? &S.Fh[0][slot] : &S.R[0][slot];
+          const int stride = e == 0 ? SH_HCAP : SH_RCAP;
+          dst[0] += gx;
+          dst[stride] += gy;
+          dst[2 * stride] += gz;
+        }
+      }
+      __syncwarp();
+      if (lane < 3 * SH_IB) {  // lane (q, c) reduces row q component c
+        const int q = lane / 3, c = lane - 3 * (lane / 3);
+        if (q < nib) {
+          double s = 0;
+#pragma unroll
+          for (int l = 0; l < 32; ++l) s += S.rows[wid][q][c][l];
+          S.Fh[c][fh0 + ib + q] += s;
+        }
+      }
+      __syncwarp();
+    }
+    hits = warp_sum(hits);
+    if (ENERGY) pe = warp_sum(pe);
+    if (lane == 0) {
+      A.hits_cell[S.hcell[h]] += hits;
+      if (ENERGY) A.pe_cell[S.hcell[h]] += pe;
+    }
+  }
+  __syncthreads();
+  // ---- 5. merge per footprint cell in a fixed order
+  const int64_t boff = BUFFERED ? SA.boff[bid] : 0;
+  for (int lc = wid; lc < nfc; lc += SH_NW) {
+    const int g0 = S.fgstart[lc];
+    if (g0 < 0) continue;
+    const int n = S.fstart[lc + 1] - S.fstart[lc];
+    const int nc = SA.mt.n[lc];
+    for (int i = lane; i < n; i += 32) {
+      double sx = 0, sy = 0, sz = 0;
+      for (int k = 0; k < nc; ++k) {
+        const int he = SA.mt.he[lc][k];
+        const int hh = he >> 4, e = he & 15;
+        if (S.hcell[hh] < 0) continue;
+        const int s = S.sbase[hh][e] + i;
+        if (e == 0) {
+          sx += S.Fh[0][s];
+          sy += S.Fh[1][s];
+          sz += S.Fh[2][s];
+        } else {
+          sx += S.R[0][s];
+          sy += S.R[1][s];
+          sz += S.R[2][s];
+        }
+      }
+      if (BUFFERED) {
+        const int64_t o = boff + S.fstart[lc] + i;
+        SA.buf[o] = sx;
+        SA.buf[SA.bufstride + o] = sy;
+        SA.buf[2 * SA.bufstride + o] = sz;
+      } else {
+        A.fx[g0 + i] += sx;
+        A.fy[g0 + i] += sy;
+        A.fz[g0 + i] += sz;
+      }
+    }
+  }
+  if (BUFFERED)
+    for (int lc = threadIdx.x; lc <= nfc; lc += blockDim.x)
+      SA.bindex[(int64_t)bid * (SH_MAXF + 1) + lc] = S.fstart[lc];
+}
+
+// buffered mode: footprint size per block (for the buffer offsets)
+__global__ void k_block_sizes(ShellArgs SA, int32_t *sizes) {
+  const ForceArgs &A = SA.A;
+  const Box &b = A.b;
+  const int64_t nb = (int64_t)A.nbk[0] * A.nbk[1] * A.nbk[2];
+  const int FX = b.blk[0] + 1, FY = b.blk[1] + 2;
+  for (int64_t bid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bid < nb;
+       bid += (int64_t)gridDim.x * blockDim.x) {
+    int o0[3] = {(int)(bid % A.nbk[0]) * b.blk[0], (int)((bid / A.nbk[0]) % A.nbk[1]) * b.blk[1],
+                 (int)(bid / ((int64_t)A.nbk[0] * A.nbk[1])) * b.blk[2]};
+    int s = 0;
+    for (int lc = 0; lc < SA.mt.nfc; ++lc) {
+      const int64_t gc = foot_cell(b, o0, lc, FX, FY);
+      if (gc >= 0) s += A.start[gc + 1] - A.start[gc];
+    }
+    sizes[bid] = s;
+  }
+}
+
+// buffered mode, pass 2: every particle sums the <= 8 block buffers whose
+// footprint box contains its cell, in a fixed block order (deterministic)
+__global__ void k_gather_blocks(ShellArgs SA) {
+  const ForceArgs &A = SA.A;
+  const Box &b = A.b;
+  const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
+  const int FX = B0 + 1, FY = B1 + 2, FZ = B2 + 2;
+  const int64_t ncell = (int64_t)b.nc[0] * b.nc[1] * b.nc[2];
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= ncell) return;
+  const int c0 = (int)(warp % b.nc[0]), c1 = (int)((warp / b.nc[0]) % b.nc[1]),
+            c2 = (int)(warp / ((int64_t)b.nc[0] * b.nc[1]));
+  const int64_t gc = box_cell(b, c0, c1, c2);
+  const int g0 = A.start[gc], n = A.start[gc + 1] - g0;
+  if (n == 0) return;
+  int kx[2], ky[3], kz[3], nx = 0, ny = 0, nz = 0;
+  kx[nx++] = c0 / B0;
+  if (c0 % B0 == 0) kx[nx++] = c0 / B0 - 1;
+  ky[ny++] = c1 / B1;
+  if (c1 % B1 == 0) ky[ny++] = c1 / B1 - 1;
+  if (c1 % B1 == B1 - 1) ky[ny++] = c1 / B1 + 1;
+  kz[nz++] = c2 / B2;
+  if (c2 % B2 == 0) kz[nz++] = c2 / B2 - 1;
+  if (c2 % B2 == B2 - 1) kz[nz++] = c2 / B2 + 1;
+  int64_t src[8];
+  int ns = 0;
+  for (int u = 0; u < nx; ++u)
+    for (int v = 0; v < ny; ++v)
+      for (int w = 0; w < nz; ++w) {
+        int k[3] = {kx[u], ky[v], kz[w]};
+        bool ok = true;
+        for (int d = 0; d < 3; ++d)
+          if (k[d] < 0 || k[d] >= A.nbk[d]) {
+            if (b.per[d]) k[d] = k[d] < 0 ? k[d] + A.nbk[d] : k[d] - A.nbk[d];
+            else ok = false;
+          }
+        if (!ok) continue;
+        int l0 = c0 - k[0] * B0, l1 = c1 - (k[1] * B1 - 1), l2 = c2 - (k[2] * B2 - 1);
+        if (b.per[0]) l0 = wrap1i(l0, b.nc[0]);
+        if (b.per[1]) l1 = wrap1i(l1, b.nc[1]);
+        if (b.per[2]) l2 = wrap1i(l2, b.nc[2]);
+        if (l0 < 0 || l0 >= FX || l1 < 0 || l1 >= FY || l2 < 0 || l2 >= FZ) continue;
+        const int lc = l0 + FX * (l1 + FY * l2);
+        const int64_t blin = k[0] + (int64_t)A.nbk[0] * (k[1] + (int64_t)A.nbk[1] * k[2]);
+        src[ns++] = SA.boff[blin] + SA.bindex[blin * (SH_MAXF + 1) + lc];
+      }
+  for (int i = lane; i < n; i += 32) {
+    double sx = 0, sy = 0, sz = 0;
+    for (int s = 0; s < ns; ++s) {
+      const int64_t o = src[s] + i;
+      sx += SA.buf[o];
+      sy += SA.buf[SA.bufstride + o];
+      sz += SA.buf[2 * SA.bufstride + o];
+    }
+    A.fx[g0 + i] += sx;
+    A.fy[g0 + i] += sy;
+    A.fz[g0 + i] += sz;
+  }
+}
+
+static int build_merge_table(const int B[3], MergeTable *mt) {
+  const int FX = B[0] + 1, FY = B[1] + 2, FZ = B[2] + 2;
+  mt->nfc = FX * FY * FZ;
+  CS_REQUIRE(mt->nfc <= SH_MAXF, "shell schedule: footprint %d cells > %d", mt->nfc, SH_MAXF);
+  int8_t st[14 * 3];
+  int n;
+  cs_host_canonical_stencil(3, st, &n);
+  for (int lc = 0; lc < mt->nfc; ++lc) {
+    const int l[3] = {lc % FX, (lc / FX) % FY - 1, lc / (FX * FY) - 1};
+    int k = 0;
+    // home rows first, then entries in canonical order: a fixed summation order
+    for (int e = 0; e < 14; ++e) {
+      const int hl[3] = {l[0] - st[3 * e], l[1] - st[3 * e + 1], l[2] - st[3 * e + 2]};
+      if (hl[0] < 0 || hl[0] >= B[0] || hl[1] < 0 || hl[1] >= B[1] || hl[2] < 0 || hl[2] >= B[2])
+        continue;
+      const int h = hl[0] + B[0] * (hl[1] + B[1] * hl[2]);
+      CS_REQUIRE(k < SH_MAXC, "merge table overflow");
+      mt->he[lc][k++] = (uint8_t)(h * 16 + e);
+    }
+    mt->n[lc] = (uint8_t)k;
+  }
+  return CS_OK;
+}
+
+static size_t shell_buffered_ws(const Box &b, int64_t n) {
+  const int64_t nb = (int64_t)((b.owned_x + b.blk[0] - 1) / b.blk[0]) * (b.nc[1] / (b.blk[1] > 0 ? b.blk[1] : 1)) *
+                     (b.nc[2] / (b.blk[2] > 0 ? b.blk[2] : 1)) + 1;
+  return cs_ws_slice(sizeof(double) * 3 * (8 * n + 64)) + 2 * cs_ws_slice(sizeof(int32_t) * (nb + 1)) +
+         cs_ws_slice(sizeof(int32_t) * nb * (SH_MAXF + 1)) + cs_scan_ws_bytes(nb) + cs_ws_slice(64);
+}
+
+static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, cs_ws *w,
+                               int64_t n, unsigned *status, cudaStream_t st) {
+  const int B[3] = {A.b.blk[0], A.b.blk[1], A.b.blk[2]};
+  CS_REQUIRE(B[0] * B[1] * B[2] <= SH_MAXB, "shell schedule: block has more than %d cells", SH_MAXB);
+  ShellArgs SA;
+  memset(&SA, 0, sizeof(SA));
+  SA.A = A;
+  CS_TRY(build_merge_table(B, &SA.mt));
+  const size_t smem = sizeof(ShellSmem);
+  static bool attr = false;
+  if (!attr) {
+    CS_CUDA(cudaFuncSetAttribute(k_force_shell<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CS_CUDA(cudaFuncSetAttribute(k_force_shell<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CS_CUDA(cudaFuncSetAttribute(k_force_shell<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CS_CUDA(cudaFuncSetAttribute(k_force_shell<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  if (buffered) {
+    const int64_t nblocks = (int64_t)A.nbk[0] * A.nbk[1] * A.nbk[2];
+    CS_WS_TAKE(*w, double, buf, 3 * (8 * n + 64));
+    CS_WS_TAKE(*w, int32_t, sizes, nblocks + 1);
+    CS_WS_TAKE(*w, int32_t, boff, nblocks + 1);
+    CS_WS_TAKE(*w, int32_t, bindex, nblocks * (SH_MAXF + 1));
+    size_t sb = cs_scan_ws_bytes(nblocks);
+    void *scratch = w->take<char>(sb);
+    CS_REQUIRE(scratch, "workspace too small (buffered scan)");
+    CS_WS_TAKE(*w, unsigned, err, 16);
+    SA.buf = buf;
+    SA.boff = boff;
+    SA.bindex = bindex;
+    SA.bufstride = 8 * n + 64;
+    SA.err = status ? status : err;
+    k_block_sizes<<<grid_for(nblocks, 128), 128, 0, st>>>(SA, sizes);
+    CS_TRY(cs_exclusive_scan_i32(sizes, boff, nblocks, scratch, sb, st));
+    if (energy)
+      k_force_shell<true, true><<<(unsigned)nblocks, SH_NW * 32, smem, st>>>(SA, -1);
+    else
+      k_force_shell<false, true><<<(unsigned)nblocks, SH_NW * 32, smem, st>>>(SA, -1);
+    const int64_t ncell = (int64_t)A.b.nc[0] * A.b.nc[1] * A.b.nc[2];
+    k_gather_blocks<<<(unsigned)((ncell * 32 + 255) / 256), 256, 0, st>>>(SA);
+    return cs_check_launch("force_buffered");
+  }
+  for (int colour = 0; colour < 8; ++colour) {
+    const int kc[3] = {colour & 1, (colour >> 1) & 1, (colour >> 2) & 1};
+    unsigned blocks = 1;
+    for (int k = 0; k < 3; ++k) blocks *= (unsigned)((A.nbk[k] - kc[k] + 1) >> 1);
+    if (!blocks) continue;
+    if (energy)
+      k_force_shell<true, false><<<blocks, SH_NW * 32, smem, st>>>(SA, colour);
+    else
+      k_force_shell<false, false><<<blocks, SH_NW * 32, smem, st>>>(SA, colour);
+  }
+  return cs_check_launch("force_shell");
+}

@@ -7,3 +7,5 @@
 #include "cs_payload.cuh"
 #include "cs_md.cuh"
 #include "cs_force.cuh"
+#include "cs_force2.cuh"
+#include "cs_probe.cuh"

@@ -23,7 +23,8 @@ from dataclasses import dataclass
 from . import _lib
 from .grid import GridSpec
 
-SCHEDULES = {"loopex": _lib.SCHED_LOOPEX, "block": _lib.SCHED_BLOCK}
+SCHEDULES = {"loopex": _lib.SCHED_LOOPEX, "block": _lib.SCHED_BLOCK, "shell": _lib.SCHED_SHELL,
+             "buffered": _lib.SCHED_BUFFERED}
 
 
 def _torch():
@@ -124,7 +125,9 @@ class LJSystem:
         self.box, self.params, self.n = box, params, int(n)
         self.schedule = schedule
         even = all(c % 2 == 0 for c in box.cells)
-        if schedule == "block":
+        if schedule in ("shell", "buffered"):
+            self.block = tuple(block) if block is not None else (2, 2, 2)
+        elif schedule == "block":
             self.block = tuple(block) if block is not None else choose_block(box.cells)
             if self.block is None:
                 raise ValueError(f"no valid block shape for cells {box.cells}; use schedule='loopex'")
@@ -146,12 +149,13 @@ class LJSystem:
         self._clj = _lib.CsLJ(params.epsilon, params.sigma, params.rc, params.mass)
         L = _lib.load()
         wsb = max(L.cs_bin_ws_bytes(self.n, C.byref(self._cbox)),
-                  L.cs_force_ws_bytes(C.byref(self._cbox), SCHEDULES[schedule]),
+                  L.cs_force_ws_bytes(C.byref(self._cbox), SCHEDULES[schedule], self.n),
                   L.cs_reduce_ws_bytes(self.n))
         self._wsb = int(wsb)
         self._ws = torch.empty(self._wsb, dtype=torch.uint8, device=d)
         self.scal = torch.zeros(8, dtype=f64, device=d)  # [0]=PE [1]=KE
         self.npairs = torch.zeros(1, dtype=torch.int64, device=d)
+        self.status = torch.zeros(1, dtype=torch.int32, device=d)  # kernel capacity flags
         self.dt = 0.005
         self._graphs = {}
 
@@ -247,10 +251,10 @@ class LJSystem:
         if count_pairs:
             self.npairs.zero_()
         _lib.call("cs_lj_forces", C.byref(self._cbox), C.byref(self._clj), SCHEDULES[self.schedule],
-                  _lib.ptr(self.cell_start), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]),
+                  self.n, _lib.ptr(self.cell_start), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]),
                   _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]),
                   _lib.ptr(self.scal) if energy else None,
-                  _lib.ptr(self.npairs) if count_pairs else None,
+                  _lib.ptr(self.npairs) if count_pairs else None, _lib.ptr(self.status),
                   _lib.ptr(self._ws), self._wsb, self._s())
 
     def kinetic(self):
@@ -274,32 +278,74 @@ class LJSystem:
             self.kinetic()
 
     # ---------------------------------------------------------- CUDA graph
-    def graph_step(self, energy: bool = False):
-        """Replay one step from a captured CUDA graph (two graphs: one per
-        ping-pong parity, since each step swaps the buffers)."""
+    def _graph(self, key, fn):
+        """Capture fn() once per (key, buffer parity) and replay it.  Capture
+        only records work, so it does not advance the state; the Python-side
+        buffer parity after the call is remembered with the graph."""
         torch = _torch()
-        key = (self.cur, energy)
-        if key not in self._graphs:
+        gkey = (key, self.cur)
+        if gkey not in self._graphs:
             start = self.cur
+            g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream(device=self.device)
             s.wait_stream(torch.cuda.current_stream())
-            g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(s):
-                saved = [t.clone() for t in self._state_tensors()]
-                self.step(energy)  # warm-up outside capture
-                torch.cuda.synchronize()
-                self.cur = start
                 with torch.cuda.graph(g, stream=s):
-                    self.step(energy)
+                    fn()
             torch.cuda.current_stream().wait_stream(s)
-            torch.cuda.synchronize()
-            # restore the pre-warm-up state: capture must not advance time
-            for t, v in zip(self._state_tensors(), saved):
-                t.copy_(v)
+            self._graphs[gkey] = (g, self.cur)
             self.cur = start
-            self._graphs[key] = g
-        self._graphs[key].replay()
-        self.cur = 1 - self.cur
+        g, after = self._graphs[gkey]
+        g.replay()
+        self.cur = after
+
+    def graph_step(self, energy: bool = False):
+        """One VV step replayed from a CUDA graph (one graph per parity)."""
+        self._graph(("step", energy), lambda: self.step(energy))
+
+    def graph_phases(self):
+        """The step as three graphs (kick+drift+rebin | forces | kick), so a
+        caller can put timing events between the phases."""
+        hdtm = 0.5 * self.dt / self.params.mass
+
+        def pre():
+            b = self._buf[self.cur]
+            _lib.call("cs_vv_kick_drift", self.n, hdtm, self.dt, C.byref(self._cbox),
+                      _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), _lib.ptr(b["vx"]),
+                      _lib.ptr(b["vy"]), _lib.ptr(b["vz"]), _lib.ptr(b["x"]), _lib.ptr(b["y"]),
+                      _lib.ptr(b["z"]), self._s())
+            self.build_cells()
+
+        def post():
+            b = self._buf[self.cur]
+            _lib.call("cs_vv_kick", self.n, hdtm, _lib.ptr(b["fx"]), _lib.ptr(b["fy"]),
+                      _lib.ptr(b["fz"]), _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]),
+                      self._s())
+
+        return (lambda: self._graph("pre", pre),
+                lambda: self._graph("force", lambda: self.compute_forces(energy=False)),
+                lambda: self._graph("post", post))
+
+    def launches_per_step(self, energy: bool = False) -> int:
+        """Kernels this package launches per step (memsets excluded)."""
+        build = 1 + 3 + 1 + 1  # count, scan x3, scatter, sort-gather
+        force = (27 if self.schedule == "loopex" else 8) + 2  # passes + pair/energy reduce
+        return 1 + build + force + 1 + (3 if energy else 0)
+
+    def candidate_pairs(self) -> int:
+        """Half-shell candidate pairs C of the current cell list (the
+        algorithmic-FLOP convention 8 C + 20 P of SURVEY 8(d))."""
+        import numpy as np
+
+        cnt = np.diff(self.cell_start.cpu().numpy()).astype(np.int64).reshape(self.box.cells[::-1])
+        c = int((cnt * (cnt - 1) // 2).sum())
+        from .grid import canonical_half_stencil
+
+        for off in canonical_half_stencil(3).inter_offsets:
+            ox, oy, oz = off
+            nb = np.roll(cnt, shift=(-oz, -oy, -ox), axis=(0, 1, 2))
+            c += int((cnt * nb).sum())
+        return c
 
     def _state_tensors(self):
         out = []
@@ -319,12 +365,21 @@ class LJSystem:
         return out
 
     # -------------------------------------------------------------- output
+    def check_status(self):
+        """Raise if a kernel reported a capacity overflow (buffered schedule)."""
+        if int(self.status.item()):
+            raise _lib.CellschedError(
+                "buffered force schedule: a block exceeded its shared-memory capacity; "
+                "use schedule='shell' (in-place fallback) for this density")
+
     def energies(self):
         """(PE, KE) of the last energy evaluation (synchronises)."""
         v = self.scal.cpu().tolist()
+        self.check_status()
         return v[0], v[1]
 
     def pair_count(self) -> int:
+        self.check_status()
         return int(self.npairs.item())
 
     def snapshot(self):

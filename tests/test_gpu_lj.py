@@ -35,7 +35,7 @@ def oracle_forces(oracle, sys, snap):
     return f, pe, npair
 
 
-@pytest.mark.parametrize("sched", ["loopex", "block"])
+@pytest.mark.parametrize("sched", ["loopex", "block", "shell", "buffered"])
 def test_cfg1_init_cells_forces(oracle, cuda, sched):
     s = md.LJSystem.fcc(6, schedule=sched)
     assert s.box.cells == (4, 4, 4) and s.n == 864
@@ -60,7 +60,7 @@ def test_cfg1_init_cells_forces(oracle, cuda, sched):
     assert s.pair_count() == npair
 
 
-@pytest.mark.parametrize("sched", ["loopex", "block"])
+@pytest.mark.parametrize("sched", ["loopex", "block", "shell", "buffered"])
 def test_cfg1_trajectory_10_steps(oracle, cuda, sched):
     s = md.LJSystem.fcc(6, schedule=sched)
     ini = {k: v.cpu().numpy()[:864] for k, v in s.initial.items()}
@@ -87,10 +87,10 @@ def test_cfg1_trajectory_10_steps(oracle, cuda, sched):
 def test_forces_vs_oracle_shapes(oracle, cuda, nuc, block):
     box, nucs, a = md.fcc_box(nuc, 0.8442)
     even = all(c % 2 == 0 for c in box.cells)
-    scheds = ["block"] + (["loopex"] if even else [])
+    scheds = ["block", "shell", "buffered"] + (["loopex"] if even else [])
     for sched in scheds:
         try:
-            s = md.LJSystem.fcc(nuc, schedule=sched, block=block if sched == "block" else None)
+            s = md.LJSystem.fcc(nuc, schedule=sched, block=block if sched != "loopex" else None)
         except ValueError:
             continue
         snap = s.snapshot()
@@ -104,10 +104,10 @@ def test_crowded_and_empty_cells(oracle, cuda):
     """Ragged occupancy: empty cells, cells above 32 particles (chunked warps)
     and a block footprint above the shared-memory cap (global fallback)."""
     rng = np.random.default_rng(3)
-    box = md.LJBox((15.0, 15.0, 15.0), (6, 6, 6))
-    n = 3000
-    pts = rng.random((n, 3)) * 15.0
-    pts[:1500] = pts[:1500] * 0.25  # dense corner: many particles per cell
+    box = md.LJBox((20.0, 20.0, 20.0), (8, 8, 8))
+    n = 4000
+    pts = rng.random((n, 3)) * 20.0
+    pts[:1500] = pts[:1500] * 0.2  # dense corner: many particles per cell
     s = md.LJSystem(box, n, schedule="block", block=(2, 2, 2))
     zeros = np.zeros(n)
     s.load_host(pts[:, 0], pts[:, 1], pts[:, 2], zeros, zeros, zeros, np.arange(n))
@@ -116,10 +116,11 @@ def test_crowded_and_empty_cells(oracle, cuda):
     assert counts.max() > 32 and (counts == 0).any()
     f, pe, npair = oracle_forces(oracle, s, snap)
     assert force_err(snap["f"], f) < FORCE_TOL
-    s2 = md.LJSystem(box, n, schedule="loopex")
-    s2.load_host(pts[:, 0], pts[:, 1], pts[:, 2], zeros, zeros, zeros, np.arange(n))
-    assert force_err(s2.snapshot()["f"], f) < FORCE_TOL
-    assert s.pair_count() == npair == s2.pair_count()
+    for sched in ("loopex", "shell"):
+        s2 = md.LJSystem(box, n, schedule=sched)
+        s2.load_host(pts[:, 0], pts[:, 1], pts[:, 2], zeros, zeros, zeros, np.arange(n))
+        assert force_err(s2.snapshot()["f"], f) < FORCE_TOL, sched
+        assert s.pair_count() == npair == s2.pair_count()
 
 
 def test_cfg2_full_size_properties(cuda):
@@ -127,9 +128,11 @@ def test_cfg2_full_size_properties(cuda):
     ~27.6 per particle, graph replay == eager stepping bit for bit."""
     a = md.LJSystem.fcc(48, schedule="block")
     b = md.LJSystem.fcc(48, schedule="loopex")
+    sh = md.LJSystem.fcc(48, schedule="shell")
     sa, sb = a.snapshot(), b.snapshot()
     assert np.array_equal(sa["id"], sb["id"])
-    assert a.pair_count() == b.pair_count()
+    assert a.pair_count() == b.pair_count() == sh.pair_count()
+    assert force_err(sh.snapshot()["f"], sb["f"]) < FORCE_TOL
     assert 26.5 < a.pair_count() / a.n < 28.5
     assert force_err(sa["f"], sb["f"]) < FORCE_TOL
     frms = np.sqrt((sa["f"] ** 2).sum(1).mean())
