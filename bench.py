@@ -314,7 +314,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--schedule", default="shell", choices=["shell", "buffered", "block", "loopex"])
+    ap.add_argument("--schedule", default="buffered", choices=["shell", "buffered", "block", "loopex"])
     ap.add_argument("--block", type=lambda s: tuple(int(v) for v in s.split(",")), default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -28,11 +28,11 @@
 #pragma once
 #include "cs_force.cuh"
 
-#define SH_NW 4        // warps per CTA; each warp runs two home cells (one per half-warp)
-#define SH_JCAP 224    // j list capacity per home cell (14 source cells)
-#define SH_JW 7        // mask words per lane (SH_JCAP / 32)
-#define SH_RCAP 1440   // reaction slots (particles) per CTA
-#define SH_HCAP 160    // home particles per CTA
+#define SH_NW 8        // warps per CTA (one home cell each for 2x2x2 blocks)
+#define SH_IB 8        // home particles per filter row block
+#define SH_JCAP 384    // j list capacity per warp (>= particles of the 14 source cells)
+#define SH_RCAP 1536   // reaction slots (particles) per CTA
+#define SH_HCAP 256    // home particles per CTA
 #define SH_MAXB 8      // home cells per CTA
 #define SH_MAXF 64     // footprint cells per CTA ((Bx+1)(By+2)(Bz+2))
 #define SH_MAXC 8      // contributors per footprint cell
@@ -44,19 +44,18 @@ struct MergeTable {              // host-built per block shape
 };
 
 struct ShellSmem {
+  double rows[SH_NW][SH_IB][3][32];  // per-lane i partials
   double R[3][SH_RCAP];              // reaction slots (e >= 1)
   double Fh[3][SH_HCAP];             // home rows (e = 0)
+  double hx[SH_NW][SH_IB][4];        // broadcast home positions
   double sh[SH_MAXB][14][3];         // image shift of source (h, e)
-  float4 jp[SH_MAXB][SH_JCAP];       // culled j: position relative to the home cell (fp32
-                                     // filter only) and the entry (e << 12 | q) as bits
-  unsigned mw[SH_NW][SH_JW][32];     // per-lane hit masks over the j list
+  int jl[SH_NW][SH_JCAP];            // culled j: entry << 24 | index in source cell
   int sstart[SH_MAXB][14];           // global start of source (h, e)
   int scount[SH_MAXB][14];           // count of source (h, e), -1: none
   int sbase[SH_MAXB][14];            // slot base (Fh for e = 0, R for e >= 1)
   int fstart[SH_MAXF + 1];           // footprint cell -> offset in the block buffer
   int fgstart[SH_MAXF];              // footprint cell -> global start (-1: none)
   int hcell[SH_MAXB];
-  int nj[SH_MAXB];
   int overflow;
 };
 
@@ -97,7 +96,7 @@ __device__ __forceinline__ int64_t foot_cell(const Box &b, const int *o0, int lc
 }
 
 template <bool ENERGY, bool BUFFERED>
-__global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int colour) {
+__global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int colour) {
   extern __shared__ __align__(16) unsigned char sh_raw[];
   ShellSmem &S = *reinterpret_cast<ShellSmem *>(sh_raw);
   const ForceArgs &A = SA.A;
@@ -156,7 +155,7 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
     S.fstart[lc + 1] = gc >= 0 ? A.start[gc + 1] - A.start[gc] : 0;
   }
   __syncthreads();
-  if (wid == 0) {  // slot bases (scan over (h, e)), capacities, footprint offsets
+  if (wid == 0) {  // slot bases (scan over (h, e)), list capacity, footprint offsets
     int fb = 0, rb = 0;
     for (int t0 = 0; t0 < nhome * 14; t0 += 32) {
       const int t = t0 + lane;
@@ -174,13 +173,11 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
       fb += __shfl_sync(CS_FULL, ih, 31);
       rb += __shfl_sync(CS_FULL, ir, 31);
     }
-    int src_max = 0, cell_max = 0;
+    int src_max = 0;
     for (int h = 0; h < nhome; ++h) {
       const int c = warp_sum(lane < 14 ? max(S.scount[h][lane], 0) : 0);
       src_max = max(src_max, c);
-      cell_max = max(cell_max, lane < 14 ? S.scount[h][lane] : 0);
     }
-    cell_max = __reduce_max_sync(CS_FULL, cell_max);
     int carry = 0;
     for (int c0 = 0; c0 < nfc; c0 += 32) {
       const int lc = c0 + lane;
@@ -196,11 +193,11 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
     }
     if (lane == 0) {
       S.fstart[0] = 0;
-      S.overflow = (fb > SH_HCAP || rb > SH_RCAP || src_max > SH_JCAP || cell_max >= 4096) ? 1 : 0;
+      S.overflow = (fb > SH_HCAP || rb > SH_RCAP || src_max > SH_JCAP) ? 1 : 0;
     }
   }
   __syncthreads();
-  if (S.overflow || B0 * B1 * B2 != 2 * SH_NW) {
+  if (S.overflow) {
     if (BUFFERED) {  // no in-place fallback in buffered mode: report to the host
       if (threadIdx.x == 0) atomicExch(SA.err, 1u);
       return;
@@ -230,203 +227,132 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
   }
   for (int i = threadIdx.x; i < SH_RCAP; i += blockDim.x) S.R[0][i] = S.R[1][i] = S.R[2][i] = 0.0;
   for (int i = threadIdx.x; i < SH_HCAP; i += blockDim.x) S.Fh[0][i] = S.Fh[1][i] = S.Fh[2][i] = 0.0;
+  __syncthreads();
 
   const double edge0 = b.L[0] / b.gnc[0], edge1 = b.L[1] / b.gnc[1], edge2 = b.L[2] / b.gnc[2];
   const double cull2 = A.p.rc2 * (1.0 + 1e-12) + 1e-12;
   const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
-  const float rc2f = (float)(A.p.rc2 + 1e-3);  // conservative fp32 prefilter bound
-
-  // ---- 1. cull + compact: half-warp per home cell (h = 2 * wid + half)
-  const int half = lane >> 4, li = lane & 15;
-  const unsigned hmask = 0xFFFFu << (16 * half);
-  const int h = 2 * wid + half;
-  const bool hvalid = S.hcell[h] >= 0;
-  const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
-  const double lo0 = (b.x0 + hg0) * edge0, lo1 = hg1 * edge1, lo2 = hg2 * edge2;
-  {
-    // exclusive prefix of the 14 source counts: lane li < 14 of each half holds source li
-    const int mycnt = (hvalid && li < 14) ? max(S.scount[h][li], 0) : 0;
-    int incl = mycnt;
-#pragma unroll
-    for (int s = 1; s < 16; s <<= 1) {
-      const int v = __shfl_up_sync(CS_FULL, incl, s, 16);
-      if (li >= s) incl += v;
-    }
-    const int excl = incl - mycnt;
-    const int total = __shfl_sync(CS_FULL, incl, 13, 16);
-    const int total_w = max(total, __shfl_xor_sync(CS_FULL, total, 16));
+  // ---- 1-4. one warp per home cell
+  for (int h = wid; h < nhome; h += SH_NW) {
+    if (S.hcell[h] < 0) continue;
+    const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
+    const int a0 = S.sstart[h][0], na = S.scount[h][0];
+    const double lo0 = (b.x0 + hg0) * edge0, lo1 = hg1 * edge1, lo2 = hg2 * edge2;
+    const double hi0 = lo0 + edge0, hi1 = lo1 + edge1, hi2 = lo2 + edge2;
+    // 1. cull + compact
     int nj = 0;
-    for (int t0 = 0; t0 < total_w; t0 += 16) {
-      const int t = t0 + li;
-      int e = 0;  // largest e with excl[e] <= t
-#pragma unroll
-      for (int st = 8; st >= 1; st >>= 1) {
-        const int cand = e + st;
-        const int ex = __shfl_sync(CS_FULL, excl, cand < 14 ? cand : 13, 16);
-        if (cand < 14 && ex <= t) e = cand;
+    for (int e = 0; e < 14; ++e) {
+      const int cn = S.scount[h][e];
+      if (cn <= 0) continue;
+      const int c0 = S.sstart[h][e];
+      const double s0 = S.sh[h][e][0], s1 = S.sh[h][e][1], s2 = S.sh[h][e][2];
+      for (int q0 = 0; q0 < cn; q0 += 32) {
+        const int q = q0 + lane;
+        bool keep = false;
+        if (q < cn) {
+          if (e == 0) {
+            keep = true;
+          } else {
+            const double xj = __ldg(A.x + c0 + q) + s0, yj = __ldg(A.y + c0 + q) + s1,
+                         zj = __ldg(A.z + c0 + q) + s2;
+            keep = box_d2(xj, lo0, hi0) + box_d2(yj, lo1, hi1) + box_d2(zj, lo2, hi2) < cull2;
+          }
+        }
+        const unsigned m = __ballot_sync(CS_FULL, keep);
+        if (keep) S.jl[wid][nj + __popc(m & ((1u << lane) - 1))] = (e << 24) | q;
+        nj += __popc(m);
       }
-      const int q = t - __shfl_sync(CS_FULL, excl, e, 16);
-      bool keep = false;
-      float4 rel;
-      if (t < total) {
-        const int gj = S.sstart[h][e] + q;
-        const double xj = __ldg(A.x + gj) + S.sh[h][e][0];
-        const double yj = __ldg(A.y + gj) + S.sh[h][e][1];
-        const double zj = __ldg(A.z + gj) + S.sh[h][e][2];
-        keep = true;  // no culling: the fp32 prefilter is cheaper than a box test
-        rel = make_float4((float)(xj - lo0), (float)(yj - lo1), (float)(zj - lo2),
-                          __int_as_float((e << 12) | q));
-      }
-      const unsigned m = (__ballot_sync(CS_FULL, keep) & hmask) >> (16 * half);
-      if (keep) S.jp[h][nj + __popc(m & ((1u << li) - 1))] = rel;
-      nj += __popc(m);
-    }
-    if (li == 0) S.nj[h] = hvalid ? nj : 0;
-  }
-  __syncthreads();  // R/Fh zeroed, lists complete
-
-  // ---- 2-4. lanes own home particles i (16 per half), F_i in registers
-  const int a0 = hvalid ? S.sstart[h][0] : 0, na = hvalid ? S.scount[h][0] : 0;
-  const int na_w = max(na, __shfl_xor_sync(CS_FULL, na, 16));
-  const int njh = S.nj[h];
-  const int nj_w = max(njh, __shfl_xor_sync(CS_FULL, njh, 16));
-  const int fh0 = S.sbase[h][0];
-  double pe = 0;
-  unsigned hits = 0;
-  for (int r = 0; r < na_w; r += 16) {
-    const int i = r + li;
-    const bool vi = i < na;
-    double xi = 0, yi = 0, zi = 0;
-    float xf = 1e30f, yf = 1e30f, zf = 1e30f;
-    if (vi) {
-      xi = __ldg(A.x + a0 + i);
-      yi = __ldg(A.y + a0 + i);
-      zi = __ldg(A.z + a0 + i);
-      xf = (float)(xi - lo0);
-      yf = (float)(yi - lo1);
-      zf = (float)(zi - lo2);
-    }
-    // 2. fp32 prefilter over the half's j list -> per-lane bit masks.  The
-    //    list starts with the home cell (entry 0, q = k for k < na), so the
-    //    intra rule j > i and the list end are one mask per word.
-    const int lim = min(i + 1, na);  // list positions k < lim are intra with q <= i
-    for (int w0 = 0; w0 < nj_w; w0 += 32) {
-      unsigned m = 0;
-#pragma unroll 8
-      for (int k = 0; k < 32; ++k) {
-        const float4 pj = S.jp[h][w0 + k];  // half-uniform address: broadcast
-        const float dx = xf - pj.x, dy = yf - pj.y, dz = zf - pj.z;
-        const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
-        m |= (unsigned)(r2 < rc2f) << k;
-      }
-      const int nv = njh - w0, nl = lim - w0;
-      const unsigned valid = nv >= 32 ? ~0u : (nv > 0 ? (1u << nv) - 1 : 0u);
-      const unsigned low = nl >= 32 ? ~0u : (nl > 0 ? (1u << nl) - 1 : 0u);
-      S.mw[wid][w0 >> 5][lane] = m & valid & ~low;
     }
     __syncwarp();
-    // 3. hit loop over the lane's own bits (uniform hit counts: ~28 per i)
-    double fxi = 0, fyi = 0, fzi = 0;
-    // lanes start their walk at staggered list positions (li * nj / 16), so
-    // two lanes rarely reach the same j in the same iteration
-    const int nwords = (nj_w + 31) >> 5;
-    const int spos = (li * njh) >> 4, sw = spos >> 5, sb = spos & 31;
-    int visit = 0, word = sw;
-    unsigned bits = vi ? (S.mw[wid][sw][lane] & (~0u << sb)) : 0u;
-    // next set bit of the lane's circular walk (false when exhausted)
-    auto next_hit = [&](int &k) -> bool {
-      while (bits == 0 && vi && visit < nwords) {
-        ++visit;
-        word = word + 1 == nwords ? 0 : word + 1;
-        bits = S.mw[wid][word][lane];
-        if (visit == nwords) bits &= (1u << sb) - 1;  // second visit of the start word
+    double pe = 0;
+    unsigned hits = 0;
+    const int fh0 = S.sbase[h][0];
+    for (int ib = 0; ib < na; ib += SH_IB) {
+      const int nib = min(SH_IB, na - ib);
+      if (lane < SH_IB) {
+        const int ii = a0 + ib + min(lane, nib - 1);
+        S.hx[wid][lane][0] = __ldg(A.x + ii);
+        S.hx[wid][lane][1] = __ldg(A.y + ii);
+        S.hx[wid][lane][2] = __ldg(A.z + ii);
       }
-      if (bits == 0) return false;
-      k = word * 32 + __ffs(bits) - 1;
-      bits &= bits - 1;
-      return true;
-    };
-    // f_ij for list position k (exact fp64); slot of the j reaction or -1
-    auto eval = [&](int k, bool ok, double &fx, double &fy, double &fz) -> int {
-      fx = fy = fz = 0.0;
-      if (!ok) return -1;
-      const int ent = __float_as_int(S.jp[h][k].w);
-      const int e = ent >> 12, q = ent & 0xFFF;
-      const int gj = S.sstart[h][e] + q;
-      const double dx = xi - (__ldg(A.x + gj) + S.sh[h][e][0]);
-      const double dy = yi - (__ldg(A.y + gj) + S.sh[h][e][1]);
-      const double dz = zi - (__ldg(A.z + gj) + S.sh[h][e][2]);
-      const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
-      if (!(r2 < rc2)) return -1;  // exact fp64 test (the fp32 filter is a superset)
-      const double rinv2 = fast_rcp(r2);
-      const double sr2 = sig2 * rinv2;
-      const double sr6 = sr2 * sr2 * sr2;
-      const double ff = eps48 * sr6 * (sr6 - 0.5) * rinv2;
-      fx = ff * dx;
-      fy = ff * dy;
-      fz = ff * dz;
-      if (ENERGY) pe += eps4 * sr6 * (sr6 - 1.0);
-      ++hits;
-      return (e == 0 ? (1 << 30) : 0) | (S.sbase[h][e] + q);
-    };
-    // reaction -f on j: unique slot per (h, e, q); two lanes of one half can
-    // hit the same j in the same step -> serialize those (rare: staggered walks)
-    auto react = [&](int slot, double fx, double fy, double fz) {
-      const unsigned peers = __match_any_sync(CS_FULL, slot);
-      if (!__any_sync(CS_FULL, slot >= 0 && __popc(peers) > 1)) {
-        if (slot >= 0) {
-          double *dst = (slot >> 30) ? &S.Fh[0][slot & ((1 << 30) - 1)] : &S.R[0][slot];
-          const int stride = (slot >> 30) ? SH_HCAP : SH_RCAP;
-          dst[0] -= fx;
-          dst[stride] -= fy;
-          dst[2 * stride] -= fz;
+#pragma unroll
+      for (int q = 0; q < SH_IB; ++q)
+        S.rows[wid][q][0][lane] = S.rows[wid][q][1][lane] = S.rows[wid][q][2][lane] = 0.0;
+      __syncwarp();
+      const unsigned qmask = (1u << nib) - 1;
+      for (int c0 = 0; c0 < nj; c0 += 32) {
+        const int jj = c0 + lane;
+        const bool vj = jj < nj;
+        const int ent = vj ? S.jl[wid][jj] : 0;
+        const int e = ent >> 24, q = ent & 0xFFFFFF;
+        double xj = 1e150, yj = 1e150, zj = 1e150;
+        if (vj) {
+          const int gj = S.sstart[h][e] + q;
+          xj = __ldg(A.x + gj) + S.sh[h][e][0];
+          yj = __ldg(A.y + gj) + S.sh[h][e][1];
+          zj = __ldg(A.z + gj) + S.sh[h][e][2];
         }
-      } else {
-        const int rank = __popc(peers & ((1u << lane) - 1));
-        const int maxr = __reduce_max_sync(CS_FULL, slot >= 0 ? __popc(peers) : 0);
-        for (int rr = 0; rr < maxr; ++rr) {
-          if (slot >= 0 && rank == rr) {
-            double *dst = (slot >> 30) ? &S.Fh[0][slot & ((1 << 30) - 1)] : &S.R[0][slot];
-            const int stride = (slot >> 30) ? SH_HCAP : SH_RCAP;
-            dst[0] -= fx;
-            dst[stride] -= fy;
-            dst[2 * stride] -= fz;
+        // intra (e == 0): only pairs i < j, i.e. rows qq < q - ib
+        const int jr = (vj && e == 0) ? q - ib : SH_IB + 1;
+        unsigned mask = 0;
+#pragma unroll
+        for (int qq = 0; qq < SH_IB; ++qq) {
+          const double dx = S.hx[wid][qq][0] - xj, dy = S.hx[wid][qq][1] - yj,
+                       dz = S.hx[wid][qq][2] - zj;
+          const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+          mask |= (unsigned)(r2 < rc2 && qq < jr) << qq;
+        }
+        mask &= qmask;
+        double gx = 0, gy = 0, gz = 0;
+        while (__any_sync(CS_FULL, mask)) {
+          if (mask) {
+            const int qq = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const double dx = S.hx[wid][qq][0] - xj, dy = S.hx[wid][qq][1] - yj,
+                         dz = S.hx[wid][qq][2] - zj;
+            const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+            const double rinv2 = fast_rcp(r2);
+            const double sr2 = sig2 * rinv2;
+            const double sr6 = sr2 * sr2 * sr2;
+            const double ff = eps48 * sr6 * (sr6 - 0.5) * rinv2;
+            const double fx = ff * dx, fy = ff * dy, fz = ff * dz;
+            gx -= fx;
+            gy -= fy;
+            gz -= fz;
+            S.rows[wid][qq][0][lane] += fx;
+            S.rows[wid][qq][1][lane] += fy;
+            S.rows[wid][qq][2][lane] += fz;
+            if (ENERGY) pe += eps4 * sr6 * (sr6 - 1.0);
+            ++hits;
           }
-          __syncwarp();
+        }
+        if (vj) {  // unique writer of slot (h, e, q)
+          const int slot = S.sbase[h][e] + q;
+          double *dst = e == 0 ? &S.Fh[0][slot] : &S.R[0][slot];
+          const int stride = e == 0 ? SH_HCAP : SH_RCAP;
+          dst[0] += gx;
+          dst[stride] += gy;
+          dst[2 * stride] += gz;
         }
       }
       __syncwarp();
-    };
-    while (true) {  // two independent hits per lane per step (ILP)
-      int k1 = 0, k2 = 0;
-      const bool a1 = next_hit(k1);
-      const bool a2 = a1 && next_hit(k2);
-      if (!__any_sync(CS_FULL, a1)) break;
-      double f1x, f1y, f1z, f2x, f2y, f2z;
-      const int s1 = eval(k1, a1, f1x, f1y, f1z);
-      const int s2 = eval(k2, a2, f2x, f2y, f2z);
-      fxi += f1x + f2x;
-      fyi += f1y + f2y;
-      fzi += f1z + f2z;
-      react(s1, f1x, f1y, f1z);
-      react(s2, f2x, f2y, f2z);
-    }
-    __syncwarp();
-    if (vi) {  // own row (intra reactions on i landed earlier, all ordered by the syncs)
-      S.Fh[0][fh0 + i] += fxi;
-      S.Fh[1][fh0 + i] += fyi;
-      S.Fh[2][fh0 + i] += fzi;
-    }
-    __syncwarp();
-  }
+      if (lane < 3 * SH_IB) {  // lane (q, c) reduces row q component c
+        const int q = lane / 3, c = lane - 3 * (lane / 3);
+        if (q < nib) {
+          double s = 0;
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {  // per home cell: half-warp sums
-    hits += __shfl_xor_sync(CS_FULL, hits, o);
-    if (ENERGY) pe += __shfl_xor_sync(CS_FULL, pe, o);
-  }
-  if (li == 0 && hvalid) {
-    A.hits_cell[S.hcell[h]] += hits;
-    if (ENERGY) A.pe_cell[S.hcell[h]] += pe;
+          for (int l = 0; l < 32; ++l) s += S.rows[wid][q][c][l];
+          S.Fh[c][fh0 + ib + q] += s;
+        }
+      }
+      __syncwarp();
+    }
+    hits = warp_sum(hits);
+    if (ENERGY) pe = warp_sum(pe);
+    if (lane == 0) {
+      A.hits_cell[S.hcell[h]] += hits;
+      if (ENERGY) A.pe_cell[S.hcell[h]] += pe;
+    }
   }
   __syncthreads();
   // ---- 5. merge per footprint cell in a fixed order
