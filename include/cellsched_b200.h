@@ -202,6 +202,31 @@ int cs_pack_plane(const cs_box *b, int plane, const int32_t *cell_start, const d
 int cs_add_plane_forces(const cs_box *b, int plane, const int32_t *cell_start, const double *in,
                         double *fx, double *fy, double *fz, void *stream);
 
+/* Slab decomposition (x-slabs, one rank per GPU).  Packed rows
+ * are [7][stride] doubles: x, y, z, vx, vy, vz, id.
+ * cs_slab_split: after the drift, split the owned particles into those that
+ * stay (packed into `stay`, stride sstride) and those that moved into the
+ * left / right neighbour's planes (packed, stride cap); counts_host[3] =
+ * {stay, left, right}.  Synchronises. */
+size_t cs_slab_ws_bytes(int64_t n);
+int cs_slab_split(int64_t n, const cs_box *b, const double *x, const double *y, const double *z,
+                  const double *vx, const double *vy, const double *vz, const int32_t *id,
+                  double *stay, int64_t sstride, double *left, double *right, int64_t cap,
+                  int64_t *counts_host, void *ws, size_t ws_bytes, void *stream);
+int cs_unpack7(int64_t m, const double *src, int64_t stride, double *x, double *y, double *z,
+               double *vx, double *vy, double *vz, int32_t *id, void *stream);
+/* cell counts of local x-plane `plane` (ny*nz cells, storage order) and its
+ * particle range [lo, hi) (range_host; synchronises) */
+int cs_plane_counts(const cs_box *b, int plane, const int32_t *cell_start, int32_t *counts,
+                    int64_t *range_host, void *stream);
+/* append the received ghost plane (counts per cell + packed positions) after
+ * the n_owned owned particles; zeroes their forces */
+size_t cs_ghost_ws_bytes(const cs_box *b);
+int cs_set_ghost_plane(const cs_box *b, int64_t n_owned, const int32_t *ghost_counts,
+                       const double *ghost_xyz, int64_t m, int32_t *cell_start, double *x,
+                       double *y, double *z, double *fx, double *fy, double *fz, void *ws,
+                       size_t ws_bytes, void *stream);
+
 /* FP64 pipe probe used by bench.py to measure the FP64 roofline peak:
  * blocks x 256 threads x iters x 256 flops (DFMA = 2 flops). */
 int cs_probe_dfma(int blocks, int iters, double *out, void *stream);

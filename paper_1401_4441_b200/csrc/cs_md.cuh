@@ -383,3 +383,186 @@ extern "C" int cs_add_plane_forces(const cs_box *bx, int plane, const int32_t *c
   if (hi > lo) k_add_plane<<<grid_for(hi - lo, 256), 256, 0, st>>>(lo, hi, in, fx, fy, fz);
   return cs_check_launch("add_plane_forces");
 }
+
+// ------------------------------------------------------- slab decomposition --
+// Particles are exchanged as packed rows [7][stride] of doubles:
+// x, y, z, vx, vy, vz, id (the id is exact in a double).
+__global__ void k_slab_code(int64_t n, Box b, const double *x, int32_t *fs, int32_t *fl,
+                            int32_t *fr) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int g = bin_coord(x[p], b.inv[0], b.gnc[0]);
+    int rel = g - b.x0;  // plane relative to the slab start, periodic in the global box
+    if (rel < 0) rel += b.gnc[0];
+    if (rel >= b.gnc[0]) rel -= b.gnc[0];
+    // owned: [0, owned_x); the right neighbour starts at owned_x; anything in the
+    // upper half of the remaining ring belongs to the left side
+    int code = 0;
+    if (rel >= b.owned_x) code = (rel - b.owned_x) < (b.gnc[0] - b.owned_x + 1) / 2 ? 2 : 1;
+    fs[p] = code == 0;
+    fl[p] = code == 1;
+    fr[p] = code == 2;
+  }
+}
+
+__global__ void k_slab_scatter(int64_t n, const int32_t *fs, const int32_t *ps, const int32_t *fl,
+                               const int32_t *pl, const int32_t *fr, const int32_t *pr,
+                               const double *x, const double *y, const double *z,
+                               const double *vx, const double *vy, const double *vz,
+                               const int32_t *id, double *stay, int64_t sstride, double *left,
+                               double *right, int64_t cap) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    double *dst;
+    int64_t o, st;
+    if (fs[p]) {
+      dst = stay; o = ps[p]; st = sstride;
+    } else if (fl[p]) {
+      dst = left; o = pl[p]; st = cap;
+      if (o >= cap) continue;
+    } else {
+      dst = right; o = pr[p]; st = cap;
+      if (o >= cap) continue;
+    }
+    dst[o] = x[p];
+    dst[st + o] = y[p];
+    dst[2 * st + o] = z[p];
+    dst[3 * st + o] = vx[p];
+    dst[4 * st + o] = vy[p];
+    dst[5 * st + o] = vz[p];
+    dst[6 * st + o] = (double)id[p];
+  }
+}
+
+extern "C" size_t cs_slab_ws_bytes(int64_t n) {
+  return 6 * cs_ws_slice(sizeof(int32_t) * (n + 1)) + cs_scan_ws_bytes(n) + cs_ws_slice(64);
+}
+
+extern "C" int cs_slab_split(int64_t n, const cs_box *bx, const double *x, const double *y,
+                             const double *z, const double *vx, const double *vy,
+                             const double *vz, const int32_t *id, double *stay, int64_t sstride,
+                             double *left, double *right, int64_t cap, int64_t *counts_host,
+                             void *ws, size_t ws_bytes, void *stream) {
+  Box b;
+  CS_TRY(make_box(bx, &b));
+  cudaStream_t st = cs_stream(stream);
+  cs_ws w(ws, ws_bytes);
+  CS_WS_TAKE(w, int32_t, fs, n + 1);
+  CS_WS_TAKE(w, int32_t, fl, n + 1);
+  CS_WS_TAKE(w, int32_t, fr, n + 1);
+  CS_WS_TAKE(w, int32_t, ps, n + 1);
+  CS_WS_TAKE(w, int32_t, pl, n + 1);
+  CS_WS_TAKE(w, int32_t, pr, n + 1);
+  size_t sb = cs_scan_ws_bytes(n);
+  void *scratch = w.take<char>(sb);
+  CS_REQUIRE(scratch, "workspace too small (slab split)");
+  if (n > 0) k_slab_code<<<grid_for(n, 256), 256, 0, st>>>(n, b, x, fs, fl, fr);
+  CS_TRY(cs_exclusive_scan_i32(fs, ps, n, scratch, sb, st));
+  CS_TRY(cs_exclusive_scan_i32(fl, pl, n, scratch, sb, st));
+  CS_TRY(cs_exclusive_scan_i32(fr, pr, n, scratch, sb, st));
+  if (n > 0)
+    k_slab_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, fs, ps, fl, pl, fr, pr, x, y, z, vx, vy,
+                                                     vz, id, stay, sstride, left, right, cap);
+  int32_t h[3];
+  CS_CUDA(cudaMemcpyAsync(&h[0], ps + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CS_CUDA(cudaMemcpyAsync(&h[1], pl + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CS_CUDA(cudaMemcpyAsync(&h[2], pr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CS_CUDA(cudaStreamSynchronize(st));
+  counts_host[0] = h[0];
+  counts_host[1] = h[1];
+  counts_host[2] = h[2];
+  if (h[1] > cap || h[2] > cap) {
+    cs_set_error("slab split: %d/%d migrants exceed the buffer capacity %lld", h[1], h[2],
+                 (long long)cap);
+    return CS_ECAPACITY;
+  }
+  return cs_check_launch("slab_split");
+}
+
+__global__ void k_unpack7(int64_t m, const double *src, int64_t stride, double *x, double *y,
+                          double *z, double *vx, double *vy, double *vz, int32_t *id) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = src[i];
+    y[i] = src[stride + i];
+    z[i] = src[2 * stride + i];
+    vx[i] = src[3 * stride + i];
+    vy[i] = src[4 * stride + i];
+    vz[i] = src[5 * stride + i];
+    id[i] = (int32_t)src[6 * stride + i];
+  }
+}
+
+extern "C" int cs_unpack7(int64_t m, const double *src, int64_t stride, double *x, double *y,
+                          double *z, double *vx, double *vy, double *vz, int32_t *id,
+                          void *stream) {
+  if (m <= 0) return CS_OK;
+  k_unpack7<<<grid_for(m, 256), 256, 0, cs_stream(stream)>>>(m, src, stride, x, y, z, vx, vy, vz, id);
+  return cs_check_launch("unpack7");
+}
+
+__global__ void k_plane_counts(int64_t c0, int64_t nplane, const int32_t *start, int32_t *cnt) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nplane;
+       c += (int64_t)gridDim.x * blockDim.x)
+    cnt[c] = start[c0 + c + 1] - start[c0 + c];
+}
+
+extern "C" int cs_plane_counts(const cs_box *bx, int plane, const int32_t *cell_start,
+                               int32_t *counts, int64_t *range_host, void *stream) {
+  Box b;
+  CS_TRY(make_box(bx, &b));
+  cudaStream_t st = cs_stream(stream);
+  int64_t lo, hi;
+  CS_TRY(plane_range(b, plane, cell_start, &lo, &hi, st));
+  const int64_t c0 = (int64_t)plane * b.stride[0];
+  k_plane_counts<<<grid_for(b.stride[0], 256), 256, 0, st>>>(c0, b.stride[0], cell_start, counts);
+  range_host[0] = lo;
+  range_host[1] = hi;
+  return cs_check_launch("plane_counts");
+}
+
+__global__ void k_ghost_start(int64_t c0, int64_t nplane, int64_t n_owned, const int32_t *gpos,
+                              int32_t *start) {
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c <= nplane;
+       c += (int64_t)gridDim.x * blockDim.x)
+    start[c0 + c] = (int32_t)(n_owned + gpos[c]);
+}
+__global__ void k_ghost_copy(int64_t m, int64_t n_owned, const double *g, double *x, double *y,
+                             double *z, double *fx, double *fy, double *fz) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[n_owned + i] = g[i];
+    y[n_owned + i] = g[m + i];
+    z[n_owned + i] = g[2 * m + i];
+    fx[n_owned + i] = 0.0;
+    fy[n_owned + i] = 0.0;
+    fz[n_owned + i] = 0.0;
+  }
+}
+
+extern "C" size_t cs_ghost_ws_bytes(const cs_box *bx) {
+  const int64_t np = (int64_t)bx->nc[1] * bx->nc[2];
+  return cs_ws_slice(sizeof(int32_t) * (np + 1)) + cs_scan_ws_bytes(np);
+}
+
+extern "C" int cs_set_ghost_plane(const cs_box *bx, int64_t n_owned, const int32_t *ghost_counts,
+                                  const double *ghost_xyz, int64_t m, int32_t *cell_start,
+                                  double *x, double *y, double *z, double *fx, double *fy,
+                                  double *fz, void *ws, size_t ws_bytes, void *stream) {
+  Box b;
+  CS_TRY(make_box(bx, &b));
+  CS_REQUIRE(!b.per[0], "ghost planes need slab (x-slowest) storage");
+  cudaStream_t st = cs_stream(stream);
+  const int64_t np = b.stride[0];
+  const int64_t c0 = (int64_t)(b.nc[0] - 1) * np;  // the ghost plane is the last local plane
+  cs_ws w(ws, ws_bytes);
+  CS_WS_TAKE(w, int32_t, gpos, np + 1);
+  size_t sb = cs_scan_ws_bytes(np);
+  void *scratch = w.take<char>(sb);
+  CS_REQUIRE(scratch, "workspace too small (ghost plane)");
+  CS_TRY(cs_exclusive_scan_i32(ghost_counts, gpos, np, scratch, sb, st));
+  k_ghost_start<<<grid_for(np + 1, 256), 256, 0, st>>>(c0, np, n_owned, gpos, cell_start);
+  if (m > 0)
+    k_ghost_copy<<<grid_for(m, 256), 256, 0, st>>>(m, n_owned, ghost_xyz, x, y, z, fx, fy, fz);
+  return cs_check_launch("set_ghost_plane");
+}

@@ -1,0 +1,394 @@
+"""x-slab decomposition of the LJ link-cell step over ranks.
+
+Rank r owns cell planes [x0, x1) of the periodic box.  All 13 half-shell
+offsets have o_x in {0, +1} (grid.py:26-33, canonical_half_stencil), so a rank
+needs exactly ONE ghost plane: the first owned plane of rank r+1 (periodic
+ring).  One force evaluation per step exchanges
+
+    positions of plane x0 -> rank r-1      (ghost positions, +L across the seam)
+    reaction forces on the ghost plane -> rank r+1   (added to its plane x0)
+
+plus particle migration after the drift.  The rank-local schedule keeps the
+same conflict-free colour passes on the local grid (x open, ghost plane last;
+SURVEY A.5).  `SlabStep` holds the protocol (order of operations, routing,
+the +L shift); an engine does the local work: `CudaSlabEngine` (C ABI kernels,
+the product) or a CPU engine in the tests.  Messages go through
+`NeighbourExchanger` (torch.distributed point-to-point: NCCL on GPUs, gloo on
+CPU).  Energies are summed with one all-reduce.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _lib
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Which x-planes a rank owns (contiguous block partition)."""
+
+    nx: int
+    world: int
+    rank: int
+
+    def __post_init__(self) -> None:
+        if not (0 <= self.rank < self.world):
+            raise ValueError("rank out of range")
+        if self.nx < self.world:
+            raise ValueError(f"{self.nx} cell planes cannot be split over {self.world} ranks")
+
+    def planes(self, r: int | None = None) -> tuple[int, int]:
+        r = self.rank if r is None else r
+        return (r * self.nx) // self.world, ((r + 1) * self.nx) // self.world
+
+    @property
+    def x0(self) -> int:
+        return self.planes()[0]
+
+    @property
+    def owned(self) -> int:
+        a, b = self.planes()
+        return b - a
+
+    @property
+    def left(self) -> int:
+        return (self.rank - 1) % self.world
+
+    @property
+    def right(self) -> int:
+        return (self.rank + 1) % self.world
+
+    def owner(self, plane: int) -> int:
+        plane %= self.nx
+        for r in range(self.world):
+            a, b = self.planes(r)
+            if a <= plane < b:
+                return r
+        raise AssertionError
+
+
+class NeighbourExchanger:
+    """Variable-size exchange with the left and right ranks of the ring.
+
+    `exchange(to_left, to_right) -> (from_left, from_right)`: sizes first, then
+    payloads, as one batch of point-to-point ops.  Leftward messages use tag
+    1, rightward tag 2, so world size 2 (left == right) is unambiguous."""
+
+    def __init__(self, layout: SlabLayout, group=None):
+        self.layout, self.group = layout, group
+
+    def exchange(self, to_left, to_right):
+        torch = _torch()
+        L = self.layout
+        if L.world == 1:
+            return to_right, to_left  # the ring closes on itself
+        import torch.distributed as dist
+
+        dev = to_left.device
+        n_send = [torch.tensor([to_left.numel()], dtype=torch.int64, device=dev),
+                  torch.tensor([to_right.numel()], dtype=torch.int64, device=dev)]
+        n_recv = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(2)]
+        self._run([(n_send[0], L.left, 1, True), (n_send[1], L.right, 2, True),
+                   (n_recv[0], L.right, 1, False), (n_recv[1], L.left, 2, False)])
+        from_right = torch.empty(int(n_recv[0].item()), dtype=to_left.dtype, device=dev)
+        from_left = torch.empty(int(n_recv[1].item()), dtype=to_left.dtype, device=dev)
+        # empty payloads are skipped on both sides (the sizes are known to both)
+        self._run([op for op in ((to_left, L.left, 1, True), (to_right, L.right, 2, True),
+                                 (from_right, L.right, 1, False), (from_left, L.left, 2, False))
+                   if op[0].numel() > 0])
+        return from_left, from_right
+
+    def _run(self, ops):
+        import torch.distributed as dist
+
+        if not ops:
+            return
+        backend = dist.get_backend(self.group)
+        if backend == "nccl":
+            p2p = [dist.P2POp(dist.isend if send else dist.irecv, t, peer, self.group, tag)
+                   for t, peer, tag, send in ops]
+            for w in dist.batch_isend_irecv(p2p):
+                w.wait()
+        else:
+            works = []
+            for t, peer, tag, send in ops:
+                fn = dist.isend if send else dist.irecv
+                works.append(fn(t, peer, group=self.group, tag=tag))
+            for w in works:
+                w.wait()
+
+    def allreduce_sum(self, values):
+        torch = _torch()
+        t = torch.tensor(values, dtype=torch.float64)
+        if self.layout.world > 1:
+            import torch.distributed as dist
+
+            if dist.get_backend(self.group) == "nccl":
+                t = t.cuda()
+            dist.all_reduce(t, group=self.group)
+        return t.cpu().tolist()
+
+
+class SlabStep:
+    """The per-rank protocol of one velocity-Verlet step (and of the initial
+    force evaluation), independent of where the local work runs."""
+
+    def __init__(self, engine, exchanger: NeighbourExchanger):
+        self.e, self.x = engine, exchanger
+
+    def migrate(self):
+        stay, to_left, to_right = self.e.split()
+        from_left, from_right = self.x.exchange(to_left, to_right)
+        self.e.assemble(stay, from_left, from_right)
+
+    def forces(self, energy: bool):
+        L = self.x.layout
+        counts, xyz = self.e.pack_first_plane(xshift=self.e.box_length_x if L.rank == 0 else 0.0)
+        # positions of my first plane go left; the right rank's first plane is my ghost
+        g_counts_l, g_counts_r = self.x.exchange(counts, counts[:0])
+        g_xyz_l, g_xyz_r = self.x.exchange(xyz, xyz[:0])
+        self.e.set_ghosts(g_counts_r, g_xyz_r)
+        pe, npairs = self.e.forces(energy)
+        # reactions on my ghost plane go back to its owner (the right rank)
+        fg = self.e.pack_ghost_forces()
+        f_from_left, _ = self.x.exchange(fg[:0], fg)
+        self.e.add_first_plane_forces(f_from_left)
+        return pe, npairs
+
+    def start(self, energy=True):
+        self.migrate()
+        self.e.build_cells()
+        pe, npairs = self.forces(energy)
+        return self._energies(pe, npairs, energy)
+
+    def step(self, energy: bool = False):
+        self.e.kick_drift()
+        self.migrate()
+        self.e.build_cells()
+        pe, npairs = self.forces(energy)
+        self.e.kick()
+        return self._energies(pe, npairs, energy)
+
+    def _energies(self, pe, npairs, energy):
+        ke = self.e.kinetic() if energy else 0.0
+        tot = self.x.allreduce_sum([pe, ke, float(npairs), float(self.e.n_owned)])
+        return {"pe": tot[0], "ke": tot[1], "pairs": int(tot[2]), "n": int(tot[3])}
+
+
+class CudaSlabEngine:
+    """Rank-local state and C ABI kernels for one x-slab on one GPU."""
+
+    def __init__(self, box, layout: SlabLayout, params, schedule="buffered", block=(2, 2, 2),
+                 capacity: int | None = None, dt: float = 0.005, device=None):
+        torch = _torch()
+        _lib.require_cuda()
+        from .md import SCHEDULES
+
+        self.box, self.layout, self.params, self.dt = box, layout, params, dt
+        self.schedule = schedule
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        nx, ny, nz = box.cells
+        owned = layout.owned
+        per_plane = max(1, int(round(4.0 * 1.0)))  # placeholder, refined below
+        dens = None
+        self.box_length_x = box.lengths[0]
+        b = _lib.CsBox()
+        b.nc[0], b.nc[1], b.nc[2] = owned + 1, ny, nz
+        b.gnc[0], b.gnc[1], b.gnc[2] = nx, ny, nz
+        b.x0 = layout.x0
+        b.owned_x = owned
+        b.periodic[0], b.periodic[1], b.periodic[2] = 0, 1, 1
+        for k in range(3):
+            b.block[k] = block[k]
+            b.L[k] = box.lengths[k]
+            b.inv[k] = box.inv[k]
+        self.cbox = b
+        self.sched = SCHEDULES[schedule]
+        self.clj = _lib.CsLJ(params.epsilon, params.sigma, params.rc, params.mass)
+        self.cap = int(capacity) if capacity else 0
+        self.n_owned = 0
+        self.n_ghost = 0
+        self.ncells_local = (owned + 1) * ny * nz
+        self.plane_cells = ny * nz
+        del per_plane, dens
+
+    # -- allocation (capacity in particles, owned + ghost) --------------------
+    def _alloc(self, cap):
+        torch = _torch()
+        d, f64 = self.device, torch.float64
+        self.cap = cap
+        mk = lambda: {k: torch.zeros(cap, dtype=f64, device=d) for k in
+                      ("x", "y", "z", "vx", "vy", "vz", "fx", "fy", "fz")}
+        self.A, self.B = mk(), mk()
+        self.A["id"] = torch.zeros(cap, dtype=torch.int32, device=d)
+        self.B["id"] = torch.zeros(cap, dtype=torch.int32, device=d)
+        self.cell_start = torch.zeros(self.ncells_local + 1, dtype=torch.int32, device=d)
+        self.mcap = max(1024, cap // 8)
+        self.P_stay = torch.zeros(7 * cap, dtype=f64, device=d)
+        self.P_l = torch.zeros(7 * self.mcap, dtype=f64, device=d)
+        self.P_r = torch.zeros(7 * self.mcap, dtype=f64, device=d)
+        L = _lib.load()
+        wsb = max(L.cs_bin_ws_bytes(cap, C.byref(self.cbox)),
+                  L.cs_force_ws_bytes(C.byref(self.cbox), self.sched, cap),
+                  L.cs_reduce_ws_bytes(cap), L.cs_slab_ws_bytes(cap),
+                  L.cs_ghost_ws_bytes(C.byref(self.cbox)))
+        self.wsb = int(wsb)
+        self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=d)
+        self.scal = torch.zeros(8, dtype=f64, device=d)
+        self.npairs = torch.zeros(1, dtype=torch.int64, device=d)
+        self.status = torch.zeros(1, dtype=torch.int32, device=d)
+        self.counts = torch.zeros(self.plane_cells, dtype=torch.int32, device=d)
+
+    def _s(self):
+        return _lib.stream_handle()
+
+    def load_global(self, x, y, z, vx, vy, vz, ids):
+        """Take this rank's particles out of global device arrays (same
+        classification kernel as the migration)."""
+        torch = _torch()
+        n = int(x.numel())
+        if self.cap == 0:
+            self._alloc(int(n / self.layout.world * 1.3) + 4 * self.plane_cells * 32 + 4096)
+        big = torch.zeros(7 * n, dtype=torch.float64, device=self.device)
+        scratch = torch.zeros(7 * n, dtype=torch.float64, device=self.device)
+        ws = torch.empty(_lib.load().cs_slab_ws_bytes(n), dtype=torch.uint8, device=self.device)
+        cnt = (C.c_int64 * 3)()
+        _lib.call("cs_slab_split", n, C.byref(self.cbox), _lib.ptr(x), _lib.ptr(y), _lib.ptr(z),
+                  _lib.ptr(vx), _lib.ptr(vy), _lib.ptr(vz), _lib.ptr(ids), _lib.ptr(big), n,
+                  _lib.ptr(scratch), _lib.ptr(scratch), n, cnt, _lib.ptr(ws), ws.numel(), self._s())
+        m = cnt[0]
+        if m > self.cap:
+            raise _lib.CellschedError("slab capacity too small for the initial load")
+        a = self.A
+        _lib.call("cs_unpack7", m, _lib.ptr(big), n, _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]),
+                  _lib.ptr(a["vx"]), _lib.ptr(a["vy"]), _lib.ptr(a["vz"]), _lib.ptr(a["id"]), self._s())
+        self.n_owned = m
+
+    # -- protocol hooks --------------------------------------------------------
+    def kick_drift(self):
+        a = self.A
+        hdtm = 0.5 * self.dt / self.params.mass
+        _lib.call("cs_vv_kick_drift", self.n_owned, hdtm, self.dt, C.byref(self.cbox),
+                  _lib.ptr(a["fx"]), _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), _lib.ptr(a["vx"]),
+                  _lib.ptr(a["vy"]), _lib.ptr(a["vz"]), _lib.ptr(a["x"]), _lib.ptr(a["y"]),
+                  _lib.ptr(a["z"]), self._s())
+
+    def kick(self):
+        a = self.A
+        hdtm = 0.5 * self.dt / self.params.mass
+        _lib.call("cs_vv_kick", self.n_owned, hdtm, _lib.ptr(a["fx"]), _lib.ptr(a["fy"]),
+                  _lib.ptr(a["fz"]), _lib.ptr(a["vx"]), _lib.ptr(a["vy"]), _lib.ptr(a["vz"]), self._s())
+
+    def split(self):
+        a = self.A
+        cnt = (C.c_int64 * 3)()
+        _lib.call("cs_slab_split", self.n_owned, C.byref(self.cbox), _lib.ptr(a["x"]), _lib.ptr(a["y"]),
+                  _lib.ptr(a["z"]), _lib.ptr(a["vx"]), _lib.ptr(a["vy"]), _lib.ptr(a["vz"]),
+                  _lib.ptr(a["id"]), _lib.ptr(self.P_stay), self.cap, _lib.ptr(self.P_l),
+                  _lib.ptr(self.P_r), self.mcap, cnt, _lib.ptr(self.ws), self.wsb, self._s())
+        self._nstay = cnt[0]
+        pack = lambda P, m, stride: P.view(7, stride)[:, :m].reshape(-1)
+        return ((self.P_stay, cnt[0], self.cap), pack(self.P_l, cnt[1], self.mcap),
+                pack(self.P_r, cnt[2], self.mcap))
+
+    def assemble(self, stay, from_left, from_right):
+        P, m, stride = stay
+        b = self.B
+        off = 0
+        for src, cnt, st in ((P, m, stride), (from_left, from_left.numel() // 7, from_left.numel() // 7),
+                             (from_right, from_right.numel() // 7, from_right.numel() // 7)):
+            if cnt == 0:
+                continue
+            if off + cnt > self.cap:
+                raise _lib.CellschedError("slab capacity exceeded by migration")
+            sl = {k: b[k][off:] for k in ("x", "y", "z", "vx", "vy", "vz", "id")}
+            _lib.call("cs_unpack7", cnt, _lib.ptr(src), st, *(_lib.ptr(sl[k]) for k in
+                      ("x", "y", "z", "vx", "vy", "vz", "id")), self._s())
+            off += cnt
+        self.n_owned = off
+        self.A, self.B = self.B, self.A  # owned particles now live in A (unsorted)
+
+    def build_cells(self):
+        a, b = self.A, self.B
+        _lib.call("cs_build_cells", self.n_owned, C.byref(self.cbox), _lib.ptr(a["x"]), _lib.ptr(a["y"]),
+                  _lib.ptr(a["z"]), _lib.ptr(a["vx"]), _lib.ptr(a["vy"]), _lib.ptr(a["vz"]),
+                  _lib.ptr(a["id"]), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]),
+                  _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]), _lib.ptr(b["id"]),
+                  _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), _lib.ptr(self.cell_start),
+                  _lib.ptr(self.ws), self.wsb, self._s())
+        self.A, self.B = self.B, self.A
+
+    def pack_first_plane(self, xshift):
+        torch = _torch()
+        rng = (C.c_int64 * 2)()
+        _lib.call("cs_plane_counts", C.byref(self.cbox), 0, _lib.ptr(self.cell_start),
+                  _lib.ptr(self.counts), rng, self._s())
+        m = rng[1] - rng[0]
+        out = torch.empty(3 * m, dtype=torch.float64, device=self.device)
+        a = self.A
+        _lib.call("cs_pack_plane", C.byref(self.cbox), 0, _lib.ptr(self.cell_start), _lib.ptr(a["x"]),
+                  _lib.ptr(a["y"]), _lib.ptr(a["z"]), float(xshift), _lib.ptr(out), self._s())
+        return self.counts.to(torch.float64), out
+
+    def set_ghosts(self, counts, xyz):
+        torch = _torch()
+        m = xyz.numel() // 3
+        if self.n_owned + m > self.cap:
+            raise _lib.CellschedError("slab capacity exceeded by the ghost plane")
+        c32 = counts.to(torch.int32).to(self.device)
+        a = self.A
+        _lib.call("cs_set_ghost_plane", C.byref(self.cbox), self.n_owned, _lib.ptr(c32),
+                  _lib.ptr(xyz.to(self.device)), m, _lib.ptr(self.cell_start), _lib.ptr(a["x"]),
+                  _lib.ptr(a["y"]), _lib.ptr(a["z"]), _lib.ptr(a["fx"]), _lib.ptr(a["fy"]),
+                  _lib.ptr(a["fz"]), _lib.ptr(self.ws), self.wsb, self._s())
+        self.n_ghost = m
+
+    def forces(self, energy):
+        a = self.A
+        self.scal[0:1].zero_()
+        self.npairs.zero_()
+        _lib.call("cs_lj_forces", C.byref(self.cbox), C.byref(self.clj), self.sched,
+                  self.n_owned + self.n_ghost, _lib.ptr(self.cell_start), _lib.ptr(a["x"]),
+                  _lib.ptr(a["y"]), _lib.ptr(a["z"]), _lib.ptr(a["fx"]), _lib.ptr(a["fy"]),
+                  _lib.ptr(a["fz"]), _lib.ptr(self.scal) if energy else None, _lib.ptr(self.npairs),
+                  _lib.ptr(self.status), _lib.ptr(self.ws), self.wsb, self._s())
+        if int(self.status.item()):
+            raise _lib.CellschedError("force kernel capacity overflow (use schedule='shell')")
+        return float(self.scal[0].item()) if energy else 0.0, int(self.npairs.item())
+
+    def pack_ghost_forces(self):
+        torch = _torch()
+        out = torch.empty(3 * self.n_ghost, dtype=torch.float64, device=self.device)
+        a = self.A
+        _lib.call("cs_pack_plane", C.byref(self.cbox), self.cbox.nc[0] - 1, _lib.ptr(self.cell_start),
+                  _lib.ptr(a["fx"]), _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), 0.0, _lib.ptr(out), self._s())
+        return out
+
+    def add_first_plane_forces(self, f):
+        a = self.A
+        _lib.call("cs_add_plane_forces", C.byref(self.cbox), 0, _lib.ptr(self.cell_start),
+                  _lib.ptr(f.to(self.device)), _lib.ptr(a["fx"]), _lib.ptr(a["fy"]), _lib.ptr(a["fz"]),
+                  self._s())
+
+    def kinetic(self):
+        a = self.A
+        _lib.call("cs_kinetic", self.n_owned, self.params.mass, _lib.ptr(a["vx"]), _lib.ptr(a["vy"]),
+                  _lib.ptr(a["vz"]), _lib.ptr(self.scal[1:]), _lib.ptr(self.ws), self.wsb, self._s())
+        return float(self.scal[1].item())
+
+    def owned_arrays(self):
+        """Host copies of the owned particles (cell-sorted): ids, x (n,3), f (n,3)."""
+        torch = _torch()
+        a, n = self.A, self.n_owned
+        return {"id": a["id"][:n].cpu().numpy(),
+                "x": torch.stack([a[k][:n] for k in ("x", "y", "z")], 1).cpu().numpy(),
+                "v": torch.stack([a[k][:n] for k in ("vx", "vy", "vz")], 1).cpu().numpy(),
+                "f": torch.stack([a[k][:n] for k in ("fx", "fy", "fz")], 1).cpu().numpy()}

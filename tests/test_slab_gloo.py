@@ -1,0 +1,234 @@
+"""Multi-rank x-slab protocol on CPU (gloo, world sizes 2 and 3).
+
+The per-rank protocol (`slab.SlabStep`: migration, ghost-plane positions to
+the left rank with +L across the seam, reaction forces back to the right
+rank, one all-reduce) is the product code; the rank-local work here is a CPU
+engine built on the oracle's half-shell task replay restricted to home cells
+in the owned planes (the same task set the CUDA engine runs).  Forces and
+energies must match the single-domain oracle."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+RHO, NUC, NSTEPS = 0.8442, 8, 6  # 8^3 FCC = 2048 particles, 5^3 cells of 2.69
+
+
+class CpuSlabEngine:
+    """Oracle-backed rank-local engine (test only)."""
+
+    def __init__(self, O, layout, cells, L, dt=0.005):
+        self.O, self.layout, self.cells, self.L, self.dt = O, layout, cells, L, dt
+        self.inv = [cells[k] / L[k] for k in range(3)]
+        self.box_length_x = L[0]
+        self.owned = layout.owned
+        self.nl = (self.owned + 1, cells[1], cells[2])  # local grid incl. ghost plane
+        st = O.canonical_stencil(3)
+        h, nb, e = O.stream_loopex(self.nl, (0, 1, 1))
+        keep = (h % self.nl[0]) < self.owned  # home cells in owned planes only
+        self.tasks = (h[keep], nb[keep], e[keep], st)
+        self.n_owned = 0
+
+    def load(self, x, v, ids):
+        gx = np.minimum((x[:, 0] * self.inv[0]).astype(int), self.cells[0] - 1)
+        rel = (gx - self.layout.x0) % self.cells[0]
+        m = rel < self.owned
+        self.x, self.v, self.id = x[m].copy(), v[m].copy(), ids[m].copy()
+        self.f = np.zeros_like(self.x)
+        self.n_owned = len(self.id)
+
+    def kick_drift(self):
+        O = self.O
+        cols = [np.ascontiguousarray(a[:, k]) for a in (self.f, self.v, self.x) for k in range(3)]
+        O.lib().o_kick(self.n_owned, 0.5 * self.dt, *cols[0:3], *cols[3:6])
+        O.lib().o_drift(self.n_owned, self.dt, np.asarray(self.L), *cols[3:6], *cols[6:9])
+        self.v = np.stack(cols[3:6], 1)
+        self.x = np.stack(cols[6:9], 1)
+
+    def kick(self):
+        cols = [np.ascontiguousarray(a[:, k]) for a in (self.f, self.v) for k in range(3)]
+        self.O.lib().o_kick(self.n_owned, 0.5 * self.dt, *cols)
+        self.v = np.stack(cols[3:6], 1)
+
+    def split(self):
+        gx = np.minimum((self.x[:, 0] * self.inv[0]).astype(int), self.cells[0] - 1)
+        rel = (gx - self.layout.x0) % self.cells[0]
+        ring = self.cells[0] - self.owned
+        code = np.where(rel < self.owned, 0, np.where(rel - self.owned < (ring + 1) // 2, 2, 1))
+        pack = lambda m: torch.from_numpy(np.concatenate(
+            [self.x[m].T, self.v[m].T, self.id[m][None].astype(np.float64)], 0).ravel().copy())
+        return (code == 0), pack(code == 1), pack(code == 2)
+
+    def assemble(self, stay, from_left, from_right):
+        parts_x, parts_v, parts_i = [self.x[stay]], [self.v[stay]], [self.id[stay]]
+        for t in (from_left, from_right):
+            a = t.numpy().reshape(7, -1)
+            parts_x.append(a[0:3].T)
+            parts_v.append(a[3:6].T)
+            parts_i.append(a[6].astype(np.int32))
+        self.x = np.concatenate(parts_x)
+        self.v = np.concatenate(parts_v)
+        self.id = np.concatenate(parts_i)
+        self.n_owned = len(self.id)
+
+    def _local_cells(self, x):
+        cx = np.minimum((x[:, 0] * self.inv[0]).astype(int), self.cells[0] - 1)
+        cx = (cx - self.layout.x0) % self.cells[0]
+        cy = np.minimum((x[:, 1] * self.inv[1]).astype(int), self.cells[1] - 1)
+        cz = np.minimum((x[:, 2] * self.inv[2]).astype(int), self.cells[2] - 1)
+        return cx, cy, cz
+
+    def build_cells(self):
+        cx, cy, cz = self._local_cells(self.x)
+        c = cx + self.nl[0] * (cy + self.nl[1] * cz)
+        o = np.lexsort((self.id, c))
+        self.x, self.v, self.id, self.c = self.x[o], self.v[o], self.id[o], c[o]
+        self.f = np.zeros_like(self.x)
+
+    def pack_first_plane(self, xshift):
+        ny, nz = self.cells[1], self.cells[2]
+        cx = self.c % self.nl[0]
+        m = cx == 0
+        plane_cell = (self.c[m] // self.nl[0])  # y + ny*z, y fastest
+        counts = np.bincount(plane_cell, minlength=ny * nz).astype(np.float64)
+        o = np.lexsort((self.id[m], plane_cell))
+        p = self.x[m][o].copy()
+        p[:, 0] += xshift
+        self._plane0 = np.nonzero(m)[0][o]
+        return torch.from_numpy(counts), torch.from_numpy(p.T.ravel().copy())
+
+    def set_ghosts(self, counts, xyz):
+        self.gx = xyz.numpy().reshape(3, -1).T.copy()
+        self.gcount = counts.numpy().astype(int)
+
+    def forces(self, energy):
+        O = self.O
+        ny, nz = self.cells[1], self.cells[2]
+        gcell = np.repeat(np.arange(ny * nz), self.gcount)
+        c_g = self.owned + self.nl[0] * gcell  # ghost plane x = owned
+        allc = np.concatenate([self.c, c_g])
+        allx = np.concatenate([self.x, self.gx])
+        o = np.argsort(allc, kind="stable")
+        xs = allx[o]
+        start = np.zeros(np.prod(self.nl) + 1, np.int32)
+        np.cumsum(np.bincount(allc, minlength=np.prod(self.nl)), out=start[1:])
+        h, nb, e, st = self.tasks
+        f, pe, npair = O.lj_tasks(list(self.nl), list(self.L), start, *(np.ascontiguousarray(xs[:, k])
+                                  for k in range(3)), h, nb, e, st, periodic=(0, 1, 1))
+        inv = np.empty_like(o)
+        inv[o] = np.arange(len(o))
+        self.f = f[inv[: self.n_owned]]
+        self.fg = f[inv[self.n_owned:]]
+        return pe, npair
+
+    def pack_ghost_forces(self):
+        return torch.from_numpy(self.fg.T.ravel().copy())
+
+    def add_first_plane_forces(self, f):
+        a = f.numpy().reshape(3, -1).T
+        self.f[self._plane0] += a
+
+    def kinetic(self):
+        return 0.5 * float((self.v ** 2).sum())
+
+
+def _worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    from paper_1401_4441_b200 import slab
+
+    a = (4 / RHO) ** (1 / 3)
+    L = [NUC * a] * 3
+    cells = [int(L[0] // 2.5)] * 3
+    x, y, z = O.fcc_positions([NUC] * 3, [a] * 3, L, 0.05, 42)
+    vx, vy, vz = O.velocities(len(x), 0.722, 1.0, 42)
+    layout = slab.SlabLayout(cells[0], world, rank)
+    eng = CpuSlabEngine(O, layout, cells, L)
+    eng.load(np.stack([x, y, z], 1), np.stack([vx, vy, vz], 1), np.arange(len(x), dtype=np.int32))
+    st = slab.SlabStep(eng, slab.NeighbourExchanger(layout))
+    out = [st.start(energy=True)]
+    f0 = (eng.id.copy(), eng.f.copy())
+    for _ in range(NSTEPS):
+        out.append(st.step(energy=True))
+    q.put((rank, out, f0, eng.id.copy(), eng.x.copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_protocol_matches_single_domain(oracle, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort(key=lambda r: r[0])
+    # single-domain reference
+    a = (4 / RHO) ** (1 / 3)
+    L = [NUC * a] * 3
+    cells = [int(L[0] // 2.5)] * 3
+    x, y, z = oracle.fcc_positions([NUC] * 3, [a] * 3, L, 0.05, 42)
+    vx, vy, vz = oracle.velocities(len(x), 0.722, 1.0, 42)
+    ref = oracle.md_run(x, y, z, vx, vy, vz, np.arange(len(x)), cells, L, NSTEPS)
+    ref0 = oracle.md_run(x, y, z, vx, vy, vz, np.arange(len(x)), cells, L, 0)
+    # initial forces, by particle id
+    ids = np.concatenate([r[2][0] for r in res])
+    fs = np.concatenate([r[2][1] for r in res])
+    assert sorted(ids.tolist()) == list(range(len(x)))
+    fref = np.empty_like(fs)
+    fref[ref0["id"]] = ref0["f"]
+    frms = np.sqrt((ref0["f"] ** 2).sum(1).mean())
+    err = np.linalg.norm(fs - fref[ids], axis=1) / np.maximum(np.linalg.norm(fref[ids], axis=1), frms)
+    assert err.max() < 1e-10
+    # energies along the trajectory (with migration across slab faces)
+    e_slab = np.array([o["pe"] + o["ke"] for o in res[0][1]])
+    e_ref = ref["pe"] + ref["ke"]
+    assert np.abs(e_slab - e_ref).max() / abs(e_ref[0]) < 1e-12
+    r0x = ref0["x"]
+    _, _, npair = oracle.lj_direct(cells, L, ref0["cell_start"], *(np.ascontiguousarray(r0x[:, k])
+                                   for k in range(3)))
+    assert res[0][1][0]["pairs"] == npair
+    assert all(r[1][-1]["n"] == len(x) for r in res)
+    # final positions by id
+    ids_f = np.concatenate([r[3] for r in res])
+    xs_f = np.concatenate([r[4] for r in res])
+    xref = np.empty_like(xs_f)
+    xref[ref["id"]] = ref["x"]
+    assert np.abs(xs_f - xref[ids_f]).max() < 1e-11
+
+
+def test_layout_logic():
+    from paper_1401_4441_b200 import slab
+
+    L = slab.SlabLayout(10, 3, 1)
+    assert L.planes(0) == (0, 3) and L.planes(1) == (3, 6) and L.planes(2) == (6, 10)
+    assert (L.left, L.right, L.x0, L.owned) == (0, 2, 3, 3)
+    assert L.owner(9) == 2 and L.owner(10) == 0 and L.owner(-1) == 2
+    with pytest.raises(ValueError):
+        slab.SlabLayout(2, 3, 0)
