@@ -56,7 +56,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
@@ -204,11 +204,90 @@ def fp64_peak(torch, lib):
     return best
 
 
+def run_slab(args, rank, ws):
+    """N > 1: x-slab decomposition, each rank owns a cfg2-sized slab (32 of
+    32N cell planes, 442,368 particles per GPU), halos/migration over NCCL."""
+    import torch
+
+    from paper_1401_4441_b200 import _lib, md, slab
+
+    dev = torch.cuda.current_device()
+    nuc = (NUC * ws, NUC, NUC)
+    box, nucs, a = md.fcc_box(nuc, 0.8442)
+    n = 4 * nucs[0] * nucs[1] * nucs[2]
+    g = md.LJSystem(box, n, schedule="loopex")  # global initial state (same on every rank)
+    g.seed_fcc(nucs, a, 0.722, 0.05, 42)
+    ini = {k: v[:n] for k, v in g.initial.items()}
+    lay = slab.SlabLayout(box.cells[0], ws, rank)
+    eng = slab.CudaSlabEngine(box, lay, md.LJParams(), schedule=args.schedule)
+    eng.load_global(ini["x"], ini["y"], ini["z"], ini["vx"], ini["vy"], ini["vz"], ini["id"])
+    del g
+    torch.cuda.empty_cache()
+    st = slab.SlabStep(eng, slab.NeighbourExchanger(lay))
+    barrier(ws)
+    st.start(energy=True)
+    for _ in range(args.warmup):
+        st.step()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    pairs = 0
+    with ClockSampler(dev) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            barrier(ws)
+            ev[k][0].record()
+            out = st.step(energy=False)
+            ev[k][1].record()
+            torch.cuda.synchronize()
+            pairs += out["pairs"]  # already summed over ranks
+    tot_s = max_over_ranks(sum(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3, ws)
+    # e2e: host buffers in, K steps with per-step energy readback, host buffers out
+    hx = {k: v.cpu().pin_memory() for k, v in ini.items()}
+    barrier(ws)
+    t0 = time.perf_counter()
+    dx = {k: v.to("cuda", non_blocking=True) for k, v in hx.items()}
+    eng2 = slab.CudaSlabEngine(box, lay, md.LJParams(), schedule=args.schedule)
+    eng2.load_global(dx["x"], dx["y"], dx["z"], dx["vx"], dx["vy"], dx["vz"], dx["id"])
+    st2 = slab.SlabStep(eng2, slab.NeighbourExchanger(lay))
+    st2.start(energy=True)
+    p2 = 0
+    for _ in range(args.steps):
+        p2 += st2.step(energy=True)["pairs"]
+    final = eng2.owned_arrays()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, ws)
+    clocks = clk.summary()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": pairs / tot_s, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded FCC + 0.05 sigma jitter, Gaussian velocities)",
+        "config": {"workload": f"cfg2 per GPU, x-slab weak scaling: FCC {nuc[0]}x48x48 = {n} particles, "
+                               f"{box.cells[0]}x32x32 cells, {lay.owned} planes per rank",
+                   "schedule": f"{args.schedule} (2, 2, 2) on the rank-local grid",
+                   "l2": "flushed (256 MB memset) between timed steps",
+                   "parallelism": f"x-slab{ws}: ghost plane + reverse forces + migration over NCCL send/recv",
+                   "steps_per_s": args.steps / tot_s},
+        "cpu_baseline": None,
+        "e2e": {"value": p2 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 52 * n / args.steps,
+                "d2h_bytes_per_step": 32 + 48 * n / args.steps},
+        "gpu_launches": args.steps * 40,
+        "clocks": clocks,
+    }
+    del final
+    print(json.dumps(line), flush=True)
+
+
 def run_ours(args):
     import numpy as np
     import torch
 
     rank, ws = dist_init()
+    if ws > 1 or args.slab:
+        return run_slab(args, rank, ws)
     from paper_1401_4441_b200 import _lib, md
 
     dev = torch.cuda.current_device()
@@ -311,12 +390,13 @@ def e2e_run(torch, md, ref_sys, args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--schedule", default="buffered", choices=["shell", "buffered", "block", "loopex"])
     ap.add_argument("--block", type=lambda s: tuple(int(v) for v in s.split(",")), default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="use the x-slab engine even at N=1")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
