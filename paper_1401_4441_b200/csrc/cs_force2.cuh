@@ -237,31 +237,30 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
     if (S.hcell[h] < 0) continue;
     const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
     const int a0 = S.sstart[h][0], na = S.scount[h][0];
-    const double lo0 = (b.x0 + hg0) * edge0, lo1 = hg1 * edge1, lo2 = hg2 * edge2;
-    const double hi0 = lo0 + edge0, hi1 = lo1 + edge1, hi2 = lo2 + edge2;
-    // 1. cull + compact
-    int nj = 0;
-    for (int e = 0; e < 14; ++e) {
-      const int cn = S.scount[h][e];
-      if (cn <= 0) continue;
-      const int c0 = S.sstart[h][e];
-      const double s0 = S.sh[h][e][0], s1 = S.sh[h][e][1], s2 = S.sh[h][e][2];
-      for (int q0 = 0; q0 < cn; q0 += 32) {
-        const int q = q0 + lane;
-        bool keep = false;
-        if (q < cn) {
-          if (e == 0) {
-            keep = true;
-          } else {
-            const double xj = __ldg(A.x + c0 + q) + s0, yj = __ldg(A.y + c0 + q) + s1,
-                         zj = __ldg(A.z + c0 + q) + s2;
-            keep = box_d2(xj, lo0, hi0) + box_d2(yj, lo1, hi1) + box_d2(zj, lo2, hi2) < cull2;
-          }
-        }
-        const unsigned m = __ballot_sync(CS_FULL, keep);
-        if (keep) S.jl[wid][nj + __popc(m & ((1u << lane) - 1))] = (e << 24) | q;
-        nj += __popc(m);
+    (void)hg0; (void)hg1; (void)hg2; (void)cull2; (void)edge0; (void)edge1; (void)edge2;
+    // 1. j list = the 14 source cells concatenated (home first).  Lanes walk
+    //    the concatenation directly (no per-cell partial warps); a box-distance
+    //    cull was measured to cost more than the candidates it removes.
+    const int mycnt = lane < 14 ? max(S.scount[h][lane], 0) : 0;
+    int incl = mycnt;
+#pragma unroll
+    for (int s = 1; s < 16; s <<= 1) {
+      const int v = __shfl_up_sync(CS_FULL, incl, s);
+      if (lane >= s) incl += v;
+    }
+    const int excl = incl - mycnt;
+    const int nj = __shfl_sync(CS_FULL, incl, 13);
+    for (int t0 = 0; t0 < nj; t0 += 32) {
+      const int t = t0 + lane;
+      int e = 0;  // largest e with excl[e] <= t
+#pragma unroll
+      for (int st = 8; st >= 1; st >>= 1) {
+        const int cand = e + st;
+        const int ex = __shfl_sync(CS_FULL, excl, cand < 14 ? cand : 13);
+        if (cand < 14 && ex <= t) e = cand;
       }
+      const int q = t - __shfl_sync(CS_FULL, excl, e);
+      if (t < nj) S.jl[wid][t] = (e << 24) | q;
     }
     __syncwarp();
     double pe = 0;
@@ -304,26 +303,47 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
         }
         mask &= qmask;
         double gx = 0, gy = 0, gz = 0;
+        // two hits per lane per step: independent dependency chains (ILP);
+        // both write different rows of this lane's private partials
         while (__any_sync(CS_FULL, mask)) {
-          if (mask) {
-            const int qq = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const double dx = S.hx[wid][qq][0] - xj, dy = S.hx[wid][qq][1] - yj,
-                         dz = S.hx[wid][qq][2] - zj;
-            const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
-            const double rinv2 = fast_rcp(r2);
-            const double sr2 = sig2 * rinv2;
-            const double sr6 = sr2 * sr2 * sr2;
-            const double ff = eps48 * sr6 * (sr6 - 0.5) * rinv2;
-            const double fx = ff * dx, fy = ff * dy, fz = ff * dz;
-            gx -= fx;
-            gy -= fy;
-            gz -= fz;
-            S.rows[wid][qq][0][lane] += fx;
-            S.rows[wid][qq][1][lane] += fy;
-            S.rows[wid][qq][2][lane] += fz;
-            if (ENERGY) pe += eps4 * sr6 * (sr6 - 1.0);
+          const bool h1 = mask != 0;
+          const int q1 = h1 ? __ffs(mask) - 1 : 0;
+          mask &= mask - 1;
+          const bool h2 = mask != 0;
+          const int q2 = h2 ? __ffs(mask) - 1 : 0;
+          mask &= mask - 1;
+          if (h1) {
+            const double dx1 = S.hx[wid][q1][0] - xj, dy1 = S.hx[wid][q1][1] - yj,
+                         dz1 = S.hx[wid][q1][2] - zj;
+            const double dx2 = S.hx[wid][q2][0] - xj, dy2 = S.hx[wid][q2][1] - yj,
+                         dz2 = S.hx[wid][q2][2] - zj;
+            const double r21 = __fma_rn(dz1, dz1, __fma_rn(dy1, dy1, dx1 * dx1));
+            const double r22 = h2 ? __fma_rn(dz2, dz2, __fma_rn(dy2, dy2, dx2 * dx2)) : 1.0;
+            const double ri1 = fast_rcp(r21), ri2 = fast_rcp(r22);
+            const double s21 = sig2 * ri1, s22 = sig2 * ri2;
+            const double s61 = s21 * s21 * s21, s62 = s22 * s22 * s22;
+            const double ff1 = eps48 * s61 * (s61 - 0.5) * ri1;
+            const double ff2 = h2 ? eps48 * s62 * (s62 - 0.5) * ri2 : 0.0;
+            const double fx1 = ff1 * dx1, fy1 = ff1 * dy1, fz1 = ff1 * dz1;
+            const double fx2 = ff2 * dx2, fy2 = ff2 * dy2, fz2 = ff2 * dz2;
+            gx -= fx1;
+            gy -= fy1;
+            gz -= fz1;
+            S.rows[wid][q1][0][lane] += fx1;
+            S.rows[wid][q1][1][lane] += fy1;
+            S.rows[wid][q1][2][lane] += fz1;
+            if (ENERGY) pe += eps4 * s61 * (s61 - 1.0);
             ++hits;
+            if (h2) {
+              gx -= fx2;
+              gy -= fy2;
+              gz -= fz2;
+              S.rows[wid][q2][0][lane] += fx2;
+              S.rows[wid][q2][1][lane] += fy2;
+              S.rows[wid][q2][2][lane] += fz2;
+              if (ENERGY) pe += eps4 * s62 * (s62 - 1.0);
+              ++hits;
+            }
           }
         }
         if (vj) {  // unique writer of slot (h, e, q)
@@ -339,10 +359,15 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
       if (lane < 3 * SH_IB) {  // lane (q, c) reduces row q component c
         const int q = lane / 3, c = lane - 3 * (lane / 3);
         if (q < nib) {
-          double s = 0;
+          double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
 #pragma unroll
-          for (int l = 0; l < 32; ++l) s += S.rows[wid][q][c][l];
-          S.Fh[c][fh0 + ib + q] += s;
+          for (int l = 0; l < 32; l += 4) {
+            s0 += S.rows[wid][q][c][l];
+            s1 += S.rows[wid][q][c][l + 1];
+            s2 += S.rows[wid][q][c][l + 2];
+            s3 += S.rows[wid][q][c][l + 3];
+          }
+          S.Fh[c][fh0 + ib + q] += (s0 + s1) + (s2 + s3);
         }
       }
       __syncwarp();
