@@ -29,10 +29,10 @@
 #include "cs_force.cuh"
 
 #define SH_NW 8        // warps per CTA (one home cell each for 2x2x2 blocks)
-#define SH_IB 8        // home particles per filter row block
+#define SH_IB 4        // home particles per filter row block
 #define SH_JCAP 384    // j list capacity per warp (>= particles of the 14 source cells)
-#define SH_RCAP 1536   // reaction slots (particles) per CTA
-#define SH_HCAP 256    // home particles per CTA
+#define SH_RCAP 1440   // reaction slots (particles) per CTA
+#define SH_HCAP 160    // home particles per CTA
 #define SH_MAXB 8      // home cells per CTA
 #define SH_MAXF 64     // footprint cells per CTA ((Bx+1)(By+2)(Bz+2))
 #define SH_MAXC 8      // contributors per footprint cell
@@ -49,7 +49,7 @@ struct ShellSmem {
   double Fh[3][SH_HCAP];             // home rows (e = 0)
   double hx[SH_NW][SH_IB][4];        // broadcast home positions
   double sh[SH_MAXB][14][3];         // image shift of source (h, e)
-  int jl[SH_NW][SH_JCAP];            // culled j: entry << 24 | index in source cell
+  uint16_t jl[SH_NW][SH_JCAP];       // j list: entry << 12 | index in source cell
   int sstart[SH_MAXB][14];           // global start of source (h, e)
   int scount[SH_MAXB][14];           // count of source (h, e), -1: none
   int sbase[SH_MAXB][14];            // slot base (Fh for e = 0, R for e >= 1)
@@ -96,7 +96,7 @@ __device__ __forceinline__ int64_t foot_cell(const Box &b, const int *o0, int lc
 }
 
 template <bool ENERGY, bool BUFFERED>
-__global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int colour) {
+__global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int colour) {
   extern __shared__ __align__(16) unsigned char sh_raw[];
   ShellSmem &S = *reinterpret_cast<ShellSmem *>(sh_raw);
   const ForceArgs &A = SA.A;
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
         if (cand < 14 && ex <= t) e = cand;
       }
       const int q = t - __shfl_sync(CS_FULL, excl, e);
-      if (t < nj) S.jl[wid][t] = (e << 24) | q;
+      if (t < nj) S.jl[wid][t] = (uint16_t)((e << 12) | q);
     }
     __syncwarp();
     double pe = 0;
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
         const int jj = c0 + lane;
         const bool vj = jj < nj;
         const int ent = vj ? S.jl[wid][jj] : 0;
-        const int e = ent >> 24, q = ent & 0xFFFFFF;
+        const int e = ent >> 12, q = ent & 0xFFF;
         double xj = 1e150, yj = 1e150, zj = 1e150;
         if (vj) {
           const int gj = S.sstart[h][e] + q;
@@ -421,83 +421,84 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
       SA.bindex[(int64_t)bid * (SH_MAXF + 1) + lc] = S.fstart[lc];
 }
 
-// buffered mode: footprint size per block (for the buffer offsets)
+// buffered mode: footprint size per block (one warp per block, lanes over cells)
 __global__ void k_block_sizes(ShellArgs SA, int32_t *sizes) {
   const ForceArgs &A = SA.A;
   const Box &b = A.b;
   const int64_t nb = (int64_t)A.nbk[0] * A.nbk[1] * A.nbk[2];
   const int FX = b.blk[0] + 1, FY = b.blk[1] + 2;
-  for (int64_t bid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; bid < nb;
-       bid += (int64_t)gridDim.x * blockDim.x) {
-    int o0[3] = {(int)(bid % A.nbk[0]) * b.blk[0], (int)((bid / A.nbk[0]) % A.nbk[1]) * b.blk[1],
-                 (int)(bid / ((int64_t)A.nbk[0] * A.nbk[1])) * b.blk[2]};
+  const int lane = threadIdx.x & 31;
+  for (int64_t bid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; bid < nb;
+       bid += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int o0[3] = {(int)(bid % A.nbk[0]) * b.blk[0], (int)((bid / A.nbk[0]) % A.nbk[1]) * b.blk[1],
+                       (int)(bid / ((int64_t)A.nbk[0] * A.nbk[1])) * b.blk[2]};
     int s = 0;
-    for (int lc = 0; lc < SA.mt.nfc; ++lc) {
+    for (int lc = lane; lc < SA.mt.nfc; lc += 32) {
       const int64_t gc = foot_cell(b, o0, lc, FX, FY);
       if (gc >= 0) s += A.start[gc + 1] - A.start[gc];
     }
-    sizes[bid] = s;
+    s = warp_sum(s);
+    if (lane == 0) sizes[bid] = s;
   }
 }
 
 // buffered mode, pass 2: every particle sums the <= 8 block buffers whose
-// footprint box contains its cell, in a fixed block order (deterministic)
+// footprint box contains its cell, in a fixed block order (deterministic).
+// One warp per cell: lanes 0..7 resolve the 2x2x2 candidate blocks once.
 __global__ void k_gather_blocks(ShellArgs SA) {
   const ForceArgs &A = SA.A;
   const Box &b = A.b;
   const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
   const int FX = B0 + 1, FY = B1 + 2, FZ = B2 + 2;
-  const int64_t ncell = (int64_t)b.nc[0] * b.nc[1] * b.nc[2];
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nc0 = b.nc[0], nc1 = b.nc[1];
+  const int ncell = nc0 * nc1 * b.nc[2];
+  const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (warp >= ncell) return;
-  const int c0 = (int)(warp % b.nc[0]), c1 = (int)((warp / b.nc[0]) % b.nc[1]),
-            c2 = (int)(warp / ((int64_t)b.nc[0] * b.nc[1]));
+  const int c0 = warp % nc0, c1 = (warp / nc0) % nc1, c2 = warp / (nc0 * nc1);
   const int64_t gc = box_cell(b, c0, c1, c2);
   const int g0 = A.start[gc], n = A.start[gc + 1] - g0;
   if (n == 0) return;
-  int kx[2], ky[3], kz[3], nx = 0, ny = 0, nz = 0;
-  kx[nx++] = c0 / B0;
-  if (c0 % B0 == 0) kx[nx++] = c0 / B0 - 1;
-  ky[ny++] = c1 / B1;
-  if (c1 % B1 == 0) ky[ny++] = c1 / B1 - 1;
-  if (c1 % B1 == B1 - 1) ky[ny++] = c1 / B1 + 1;
-  kz[nz++] = c2 / B2;
-  if (c2 % B2 == 0) kz[nz++] = c2 / B2 - 1;
-  if (c2 % B2 == B2 - 1) kz[nz++] = c2 / B2 + 1;
-  int64_t src[8];
-  int ns = 0;
-  for (int u = 0; u < nx; ++u)
-    for (int v = 0; v < ny; ++v)
-      for (int w = 0; w < nz; ++w) {
-        int k[3] = {kx[u], ky[v], kz[w]};
-        bool ok = true;
-        for (int d = 0; d < 3; ++d)
-          if (k[d] < 0 || k[d] >= A.nbk[d]) {
-            if (b.per[d]) k[d] = k[d] < 0 ? k[d] + A.nbk[d] : k[d] - A.nbk[d];
-            else ok = false;
-          }
-        if (!ok) continue;
-        int l0 = c0 - k[0] * B0, l1 = c1 - (k[1] * B1 - 1), l2 = c2 - (k[2] * B2 - 1);
-        if (b.per[0]) l0 = wrap1i(l0, b.nc[0]);
-        if (b.per[1]) l1 = wrap1i(l1, b.nc[1]);
-        if (b.per[2]) l2 = wrap1i(l2, b.nc[2]);
-        if (l0 < 0 || l0 >= FX || l1 < 0 || l1 >= FY || l2 < 0 || l2 >= FZ) continue;
-        const int lc = l0 + FX * (l1 + FY * l2);
-        const int64_t blin = k[0] + (int64_t)A.nbk[0] * (k[1] + (int64_t)A.nbk[1] * k[2]);
-        src[ns++] = SA.boff[blin] + SA.bindex[blin * (SH_MAXF + 1) + lc];
+  // per axis: the block containing c and, at a block edge, the neighbour
+  // block whose footprint reaches c (x: footprint reaches +1; y, z: -1, +B)
+  int src = -1;
+  if (lane < 8) {
+    const int u = lane & 1, v = (lane >> 1) & 1, w = lane >> 2;
+    int k0 = c0 / B0, k1 = c1 / B1, k2 = c2 / B2;
+    bool ok = true;
+    if (u) { if (c0 % B0 == 0) k0 -= 1; else ok = false; }
+    if (v) { if (c1 % B1 == 0) k1 -= 1; else if (c1 % B1 == B1 - 1) k1 += 1; else ok = false; }
+    if (w) { if (c2 % B2 == 0) k2 -= 1; else if (c2 % B2 == B2 - 1) k2 += 1; else ok = false; }
+    if (k0 < 0 || k0 >= A.nbk[0]) { if (b.per[0]) k0 = wrap1i(k0, A.nbk[0]); else ok = false; }
+    if (k1 < 0 || k1 >= A.nbk[1]) { if (b.per[1]) k1 = wrap1i(k1, A.nbk[1]); else ok = false; }
+    if (k2 < 0 || k2 >= A.nbk[2]) { if (b.per[2]) k2 = wrap1i(k2, A.nbk[2]); else ok = false; }
+    if (ok) {
+      int l0 = c0 - k0 * B0, l1 = c1 - (k1 * B1 - 1), l2 = c2 - (k2 * B2 - 1);
+      if (b.per[0]) l0 = wrap1i(l0, nc0);
+      if (b.per[1]) l1 = wrap1i(l1, nc1);
+      if (b.per[2]) l2 = wrap1i(l2, b.nc[2]);
+      if (l0 >= 0 && l0 < FX && l1 >= 0 && l1 < FY && l2 >= 0 && l2 < FZ) {
+        const int blin = k0 + A.nbk[0] * (k1 + A.nbk[1] * k2);
+        src = SA.boff[blin] + SA.bindex[(int64_t)blin * (SH_MAXF + 1) + l0 + FX * (l1 + FY * l2)];
       }
-  for (int i = lane; i < n; i += 32) {
-    double sx = 0, sy = 0, sz = 0;
-    for (int s = 0; s < ns; ++s) {
-      const int64_t o = src[s] + i;
-      sx += SA.buf[o];
-      sy += SA.buf[SA.bufstride + o];
-      sz += SA.buf[2 * SA.bufstride + o];
     }
-    A.fx[g0 + i] += sx;
-    A.fy[g0 + i] += sy;
-    A.fz[g0 + i] += sz;
+  }
+  const unsigned have = __ballot_sync(CS_FULL, src >= 0);
+  for (int i = lane; i < ((n + 31) & ~31); i += 32) {
+    double sx = 0, sy = 0, sz = 0;
+    for (unsigned m = have; m; m &= m - 1) {
+      const int o = __shfl_sync(CS_FULL, src, __ffs(m) - 1) + i;
+      if (i < n) {
+        sx += SA.buf[o];
+        sy += SA.buf[SA.bufstride + o];
+        sz += SA.buf[2 * SA.bufstride + o];
+      }
+    }
+    if (i < n) {
+      A.fx[g0 + i] += sx;
+      A.fy[g0 + i] += sy;
+      A.fz[g0 + i] += sz;
+    }
   }
 }
 
@@ -564,7 +565,7 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, c
     SA.bindex = bindex;
     SA.bufstride = 8 * n + 64;
     SA.err = status ? status : err;
-    k_block_sizes<<<grid_for(nblocks, 128), 128, 0, st>>>(SA, sizes);
+    k_block_sizes<<<grid_for(nblocks * 32, 256), 256, 0, st>>>(SA, sizes);
     CS_TRY(cs_exclusive_scan_i32(sizes, boff, nblocks, scratch, sb, st));
     if (energy)
       k_force_shell<true, true><<<(unsigned)nblocks, SH_NW * 32, smem, st>>>(SA, -1);
