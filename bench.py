@@ -34,6 +34,15 @@ NUC = 48  # cfg2
 WORKLOAD = "cfg2: LJ fluid FCC 48^3 = 442368 particles, rho* 0.8442, T* 0.722, rc 2.5 (unshifted), 32^3 cells, dt 0.005, fp64, 1 VV step"
 
 
+def traffic_bytes():
+    """DRAM bytes per force launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return json.load(f)["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -343,8 +352,8 @@ def run_ours(args):
                    "force_ms_per_step": statistics.mean(force_ms), "force_share": sum(force_ms) / sum(step_ms),
                    "parallelism": f"dp{ws}" if ws > 1 else "single"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
-                     "frac": achieved / peak_fp64, "traffic": None,
-                     "kernel": "k_force_block (8 colour passes)",
+                     "frac": achieved / peak_fp64, "traffic": traffic_bytes(),
+                     "kernel": f"k_force_shell ({args.schedule} schedule)",
                      "flops_convention": "8 C + 20 P per force evaluation (SURVEY 8d)",
                      "peak_source": "measured live: cs_probe_dfma DFMA chains (MEASURED_PEAKS.json has no FP64 entry)",
                      "hbm_peak_gbs": peaks().get("hbm_gbs")},
