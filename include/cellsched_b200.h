@@ -98,6 +98,26 @@ int cs_stream_depth(const cs_grid *g, int strategy, int n, int64_t ntasks, const
                     int32_t *level, int method, int64_t *depth_host, void *ws, size_t ws_bytes,
                     void *stream);
 
+/* Generic task lists (any resources, read-only inputs): detect_dependencies
+ * with the full _DependenceState rule (depgraph.py:28-49).  Accesses in
+ * stream order (task-major; a task's reads before its writes; reads of a
+ * resource the task also writes dropped), tptr[ntasks+1] = access ranges.
+ * Pass 1 returns the edge count (synchronises); pass 2, called next with
+ * the same workspace, writes eu/ev sorted by (succ, pred).  npred_max bounds
+ * the raw predecessor total (2 * nacc is always enough). */
+size_t cs_detect_ws_bytes(int64_t ntasks, int64_t nacc, int64_t npred_max);
+int cs_detect_generic(int64_t ntasks, int64_t nacc, int64_t nres, const int64_t *tptr,
+                      const int32_t *acc_task, const int32_t *acc_res, const uint8_t *acc_write,
+                      int64_t npred_max, int64_t *nedges_host, void *ws, size_t ws_bytes,
+                      void *stream);
+int cs_detect_generic_emit(int64_t ntasks, int64_t nacc, const int64_t *tptr, int64_t npred_max,
+                           int64_t *eu, int64_t *ev, void *ws, size_t ws_bytes, void *stream);
+/* critical_path of any forward edge list sorted by succ (depgraph.py:160-174);
+ * CS_ECYCLE on a non-forward edge (depgraph.py:170-171).  Synchronises. */
+size_t cs_longest_path_ws_bytes(int64_t ntasks);
+int cs_longest_path(int64_t ntasks, int64_t nedges, const int64_t *eu, const int64_t *ev,
+                    int32_t *level, int64_t *depth_host, void *ws, size_t ws_bytes, void *stream);
+
 /* ===================== K5: integer payload (parity harness) ============== */
 /* charges (payload.py:58-61): q[cell] */
 int cs_payload_charges(const cs_grid *g, int64_t seed, int64_t *q, void *stream);
@@ -112,6 +132,15 @@ int cs_payload_levels(const cs_grid *g, const int64_t *q, int64_t ntasks, const 
                       const int32_t *nbr, const int16_t *entry, const int8_t *entry_offsets_host,
                       int n, const int32_t *level, int64_t depth, int64_t *acc, void *ws,
                       size_t ws_bytes, void *stream);
+/* apply_tasks for any task list (payload.py:84-119): kind 0 intra (val[w0] +=
+ * intra), 1 inter (val[w0] += g, val[w1] -= g; accumulator or buffer slots),
+ * 2 reduce (val[w0] += sum val[reads]); executed level by level. */
+size_t cs_payload_generic_ws_bytes(int64_t ntasks, int64_t depth);
+int cs_payload_generic(int64_t ntasks, int dim, const int8_t *kind, const int32_t *home,
+                       const int32_t *nbr, const int32_t *w0, const int32_t *w1, const int8_t *off,
+                       const int64_t *rptr, const int32_t *rres, const int64_t *q,
+                       const int32_t *level, int64_t depth, int64_t nres, int64_t *val, void *ws,
+                       size_t ws_bytes, void *stream);
 /* The colour-pass schedules of the LJ kernel, run on the integer payload:
  * sched CS_SCHED_LOOPEX (27 passes) or CS_SCHED_BLOCK (8 block passes).
  * race_check != 0 records writers per pass and fails with CS_ECONFLICT. */

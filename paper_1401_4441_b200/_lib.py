@@ -88,6 +88,13 @@ _SIGS = {
     "cs_pack_plane": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _D, _P, _P]),
     "cs_add_plane_forces": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P]),
     "cs_probe_dfma": (C.c_int, [C.c_int, C.c_int, _P, _P]),
+    "cs_detect_ws_bytes": (_SZ, [_I64, _I64, _I64]),
+    "cs_detect_generic": (C.c_int, [_I64, _I64, _I64, _P, _P, _P, _P, _I64, _P, _P, _SZ, _P]),
+    "cs_detect_generic_emit": (C.c_int, [_I64, _I64, _P, _I64, _P, _P, _P, _SZ, _P]),
+    "cs_longest_path_ws_bytes": (_SZ, [_I64]),
+    "cs_longest_path": (C.c_int, [_I64, _I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "cs_payload_generic_ws_bytes": (_SZ, [_I64, _I64]),
+    "cs_payload_generic": (C.c_int, [_I64, C.c_int] + [_P] * 10 + [_I64, _I64, _P, _P, _SZ, _P]),
     "cs_slab_ws_bytes": (_SZ, [_I64]),
     "cs_slab_split": (C.c_int, [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _SZ, _P]),
     "cs_unpack7": (C.c_int, [_I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
