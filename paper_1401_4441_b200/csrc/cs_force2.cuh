@@ -29,7 +29,9 @@
 #include "cs_force.cuh"
 
 #define SH_NW 8        // warps per CTA (one home cell each for 2x2x2 blocks)
-#define SH_IB 4        // home particles per filter row block
+#define SH_IB 16       // home particles per row block (= i-owner lanes)
+#define SH_FB 128      // hit window: forces staged per warp
+#define SH_DCAP 512    // hit descriptors per chunk (32 j x 16 i)
 #define SH_JCAP 384    // j list capacity per warp (>= particles of the 14 source cells)
 #define SH_RCAP 1440   // reaction slots (particles) per CTA
 #define SH_HCAP 160    // home particles per CTA
@@ -44,10 +46,14 @@ struct MergeTable {              // host-built per block shape
 };
 
 struct ShellSmem {
-  double rows[SH_NW][SH_IB][3][32];  // per-lane i partials
   double R[3][SH_RCAP];              // reaction slots (e >= 1)
   double Fh[3][SH_HCAP];             // home rows (e = 0)
-  double hx[SH_NW][SH_IB][4];        // broadcast home positions
+  double hxd[SH_NW][SH_IB][4];       // home positions (fp64, exact re-test)
+  float4 hxf[SH_NW][SH_IB];          // home positions relative to the cell (fp32 filter)
+  double fb[SH_NW][3][SH_FB];        // forces of the current hit window
+  uint16_t desc[SH_NW][SH_DCAP];     // hit descriptors (j lane << 5 | i), j-major
+  int seg[SH_NW][32];                // lane j: first descriptor of its hits
+  unsigned msk[SH_NW][32];           // lane j: hit mask over the row block
   double sh[SH_MAXB][14][3];         // image shift of source (h, e)
   uint16_t jl[SH_NW][SH_JCAP];       // j list: entry << 12 | index in source cell
   int sstart[SH_MAXB][14];           // global start of source (h, e)
@@ -96,7 +102,7 @@ __device__ __forceinline__ int64_t foot_cell(const Box &b, const int *o0, int lc
 }
 
 template <bool ENERGY, bool BUFFERED>
-__global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int colour) {
+__global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int colour) {
   extern __shared__ __align__(16) unsigned char sh_raw[];
   ShellSmem &S = *reinterpret_cast<ShellSmem *>(sh_raw);
   const ForceArgs &A = SA.A;
@@ -232,15 +238,16 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
   const double edge0 = b.L[0] / b.gnc[0], edge1 = b.L[1] / b.gnc[1], edge2 = b.L[2] / b.gnc[2];
   const double cull2 = A.p.rc2 * (1.0 + 1e-12) + 1e-12;
   const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
+  const float rc2f = (float)(rc2 + 1e-3);  // conservative fp32 prefilter bound (exact fp64 re-test)
   // ---- 1-4. one warp per home cell
   for (int h = wid; h < nhome; h += SH_NW) {
     if (S.hcell[h] < 0) continue;
     const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
     const int a0 = S.sstart[h][0], na = S.scount[h][0];
-    (void)hg0; (void)hg1; (void)hg2; (void)cull2; (void)edge0; (void)edge1; (void)edge2;
-    // 1. j list = the 14 source cells concatenated (home first).  Lanes walk
-    //    the concatenation directly (no per-cell partial warps); a box-distance
-    //    cull was measured to cost more than the candidates it removes.
+    const double lo0 = (b.x0 + hg0) * edge0, lo1 = hg1 * edge1, lo2 = hg2 * edge2;
+    (void)cull2;
+    // 1. j list = the 14 source cells concatenated (home first); lanes walk
+    //    the concatenation directly
     const int mycnt = lane < 14 ? max(S.scount[h][lane], 0) : 0;
     int incl = mycnt;
 #pragma unroll
@@ -270,15 +277,15 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
       const int nib = min(SH_IB, na - ib);
       if (lane < SH_IB) {
         const int ii = a0 + ib + min(lane, nib - 1);
-        S.hx[wid][lane][0] = __ldg(A.x + ii);
-        S.hx[wid][lane][1] = __ldg(A.y + ii);
-        S.hx[wid][lane][2] = __ldg(A.z + ii);
+        const double x = __ldg(A.x + ii), y = __ldg(A.y + ii), z = __ldg(A.z + ii);
+        S.hxd[wid][lane][0] = x;
+        S.hxd[wid][lane][1] = y;
+        S.hxd[wid][lane][2] = z;
+        S.hxf[wid][lane] = make_float4((float)(x - lo0), (float)(y - lo1), (float)(z - lo2), 0.f);
       }
-#pragma unroll
-      for (int q = 0; q < SH_IB; ++q)
-        S.rows[wid][q][0][lane] = S.rows[wid][q][1][lane] = S.rows[wid][q][2][lane] = 0.0;
       __syncwarp();
       const unsigned qmask = (1u << nib) - 1;
+      double fix = 0, fiy = 0, fiz = 0;  // F_i of i-owner lane (i = ib + lane, lane < nib)
       for (int c0 = 0; c0 < nj; c0 += 32) {
         const int jj = c0 + lane;
         const bool vj = jj < nj;
@@ -291,62 +298,101 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
           yj = __ldg(A.y + gj) + S.sh[h][e][1];
           zj = __ldg(A.z + gj) + S.sh[h][e][2];
         }
-        // intra (e == 0): only pairs i < j, i.e. rows qq < q - ib
-        const int jr = (vj && e == 0) ? q - ib : SH_IB + 1;
-        unsigned mask = 0;
+        // 2. fp32 prefilter: 16 rows against this lane's j
+        const float xf = (float)(xj - lo0), yf = (float)(yj - lo1), zf = (float)(zj - lo2);
+        unsigned m = 0;
 #pragma unroll
         for (int qq = 0; qq < SH_IB; ++qq) {
-          const double dx = S.hx[wid][qq][0] - xj, dy = S.hx[wid][qq][1] - yj,
-                       dz = S.hx[wid][qq][2] - zj;
-          const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
-          mask |= (unsigned)(r2 < rc2 && qq < jr) << qq;
+          const float4 p = S.hxf[wid][qq];
+          const float dx = p.x - xf, dy = p.y - yf, dz = p.z - zf;
+          m |= (unsigned)(__fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx)) < rc2f) << qq;
         }
-        mask &= qmask;
-        double gx = 0, gy = 0, gz = 0;
-        // two hits per lane per step: independent dependency chains (ILP);
-        // both write different rows of this lane's private partials
-        while (__any_sync(CS_FULL, mask)) {
-          const bool h1 = mask != 0;
-          const int q1 = h1 ? __ffs(mask) - 1 : 0;
-          mask &= mask - 1;
-          const bool h2 = mask != 0;
-          const int q2 = h2 ? __ffs(mask) - 1 : 0;
-          mask &= mask - 1;
-          if (h1) {
-            const double dx1 = S.hx[wid][q1][0] - xj, dy1 = S.hx[wid][q1][1] - yj,
-                         dz1 = S.hx[wid][q1][2] - zj;
-            const double dx2 = S.hx[wid][q2][0] - xj, dy2 = S.hx[wid][q2][1] - yj,
-                         dz2 = S.hx[wid][q2][2] - zj;
-            const double r21 = __fma_rn(dz1, dz1, __fma_rn(dy1, dy1, dx1 * dx1));
-            const double r22 = h2 ? __fma_rn(dz2, dz2, __fma_rn(dy2, dy2, dx2 * dx2)) : 1.0;
-            const double ri1 = fast_rcp(r21), ri2 = fast_rcp(r22);
-            const double s21 = sig2 * ri1, s22 = sig2 * ri2;
-            const double s61 = s21 * s21 * s21, s62 = s22 * s22 * s22;
-            const double ff1 = eps48 * s61 * (s61 - 0.5) * ri1;
-            const double ff2 = h2 ? eps48 * s62 * (s62 - 0.5) * ri2 : 0.0;
-            const double fx1 = ff1 * dx1, fy1 = ff1 * dy1, fz1 = ff1 * dz1;
-            const double fx2 = ff2 * dx2, fy2 = ff2 * dy2, fz2 = ff2 * dz2;
-            gx -= fx1;
-            gy -= fy1;
-            gz -= fz1;
-            S.rows[wid][q1][0][lane] += fx1;
-            S.rows[wid][q1][1][lane] += fy1;
-            S.rows[wid][q1][2][lane] += fz1;
-            if (ENERGY) pe += eps4 * s61 * (s61 - 1.0);
-            ++hits;
-            if (h2) {
-              gx -= fx2;
-              gy -= fy2;
-              gz -= fz2;
-              S.rows[wid][q2][0][lane] += fx2;
-              S.rows[wid][q2][1][lane] += fy2;
-              S.rows[wid][q2][2][lane] += fz2;
-              if (ENERGY) pe += eps4 * s62 * (s62 - 1.0);
-              ++hits;
-            }
+        if (e == 0) m &= (q - ib <= 0) ? 0u : (q - ib >= SH_IB ? 0xFFFFu : ((1u << (q - ib)) - 1));
+        m = vj ? (m & qmask) : 0u;
+        // 3. j-major compaction of the hits into descriptors
+        const int cnt = __popc(m);
+        int ci = cnt;
+#pragma unroll
+        for (int s = 1; s < 32; s <<= 1) {
+          const int v = __shfl_up_sync(CS_FULL, ci, s);
+          if (lane >= s) ci += v;
+        }
+        const int seg = ci - cnt;
+        const int T = __shfl_sync(CS_FULL, ci, 31);
+        if (T == 0) continue;
+        S.seg[wid][lane] = seg;
+        S.msk[wid][lane] = m;
+        {
+          unsigned mm = m;
+          int r = seg;
+          while (mm) {
+            const int qq = __ffs(mm) - 1;
+            mm &= mm - 1;
+            S.desc[wid][r++] = (uint16_t)((lane << 5) | qq);
           }
         }
-        if (vj) {  // unique writer of slot (h, e, q)
+        // transposed rows: bit jl of rowm = hit (i = lane, j = lane jl)
+        unsigned rowm = 0;
+#pragma unroll
+        for (int qq = 0; qq < SH_IB; ++qq) {
+          const unsigned bq = __ballot_sync(CS_FULL, (m >> qq) & 1u);
+          if (lane == qq) rowm = bq;
+        }
+        __syncwarp();
+        double gx = 0, gy = 0, gz = 0;  // reaction on this lane's j
+        for (int w0 = 0; w0 < T; w0 += SH_FB) {  // hit windows (one in practice)
+          const int wn = min(SH_FB, T - w0);
+          for (int t0 = 0; t0 < wn; t0 += 32) {  // dense rounds: every lane one hit
+            const int t = t0 + lane;
+            const bool act = t < wn;
+            const int d = act ? S.desc[wid][w0 + t] : 0;
+            const int jl = d >> 5, qq = d & 31;
+            const double xjl = __shfl_sync(CS_FULL, xj, jl), yjl = __shfl_sync(CS_FULL, yj, jl),
+                         zjl = __shfl_sync(CS_FULL, zj, jl);
+            double fx = 0, fy = 0, fz = 0;
+            if (act) {
+              const double dx = S.hxd[wid][qq][0] - xjl, dy = S.hxd[wid][qq][1] - yjl,
+                           dz = S.hxd[wid][qq][2] - zjl;
+              const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+              if (r2 < rc2) {  // exact test (same expression as the oracle)
+                const double rinv2 = fast_rcp(r2);
+                const double sr2 = sig2 * rinv2;
+                const double sr6 = sr2 * sr2 * sr2;
+                const double ff = eps48 * sr6 * (sr6 - 0.5) * rinv2;
+                fx = ff * dx;
+                fy = ff * dy;
+                fz = ff * dz;
+                if (ENERGY) pe += eps4 * sr6 * (sr6 - 1.0);
+                ++hits;
+              }
+              S.fb[wid][0][t] = fx;
+              S.fb[wid][1][t] = fy;
+              S.fb[wid][2][t] = fz;
+            }
+          }
+          __syncwarp();
+          // F_j: this lane's hits are the contiguous descriptors [seg, seg+cnt)
+          const int lo = max(seg, w0), hi = min(seg + cnt, w0 + wn);
+          for (int t = lo; t < hi; ++t) {
+            gx -= S.fb[wid][0][t - w0];
+            gy -= S.fb[wid][1][t - w0];
+            gz -= S.fb[wid][2][t - w0];
+          }
+          // F_i: i-owner lanes walk their row bits
+          if (lane < nib) {
+            for (unsigned mm = rowm; mm; mm &= mm - 1) {
+              const int jl = __ffs(mm) - 1;
+              const int pos = S.seg[wid][jl] + __popc(S.msk[wid][jl] & ((1u << lane) - 1)) - w0;
+              if (pos >= 0 && pos < wn) {
+                fix += S.fb[wid][0][pos];
+                fiy += S.fb[wid][1][pos];
+                fiz += S.fb[wid][2][pos];
+              }
+            }
+          }
+          __syncwarp();
+        }
+        if (cnt) {  // unique writer of slot (h, e, q)
           const int slot = S.sbase[h][e] + q;
           double *dst = e == 0 ? &S.Fh[0][slot] : &S.R[0][slot];
           const int stride = e == 0 ? SH_HCAP : SH_RCAP;
@@ -354,21 +400,12 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
           dst[stride] += gy;
           dst[2 * stride] += gz;
         }
+        __syncwarp();
       }
-      __syncwarp();
-      if (lane < 3 * SH_IB) {  // lane (q, c) reduces row q component c
-        const int q = lane / 3, c = lane - 3 * (lane / 3);
-        if (q < nib) {
-          double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-#pragma unroll
-          for (int l = 0; l < 32; l += 4) {
-            s0 += S.rows[wid][q][c][l];
-            s1 += S.rows[wid][q][c][l + 1];
-            s2 += S.rows[wid][q][c][l + 2];
-            s3 += S.rows[wid][q][c][l + 3];
-          }
-          S.Fh[c][fh0 + ib + q] += (s0 + s1) + (s2 + s3);
-        }
+      if (lane < nib) {  // own row (after this row block's intra reactions)
+        S.Fh[0][fh0 + ib + lane] += fix;
+        S.Fh[1][fh0 + ib + lane] += fiy;
+        S.Fh[2][fh0 + ib + lane] += fiz;
       }
       __syncwarp();
     }
