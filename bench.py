@@ -301,7 +301,7 @@ def run_ours(args):
 
     dev = torch.cuda.current_device()
     peak_fp64 = fp64_peak(torch, _lib)
-    sysm = md.LJSystem.fcc(NUC, schedule=args.schedule, block=args.block, seed=42 + rank)
+    sysm = md.LJSystem.fcc(NUC, schedule=args.schedule, block=args.block, seed=42 + rank, skin=args.skin)
     pre, force, post = sysm.graph_phases()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(args.warmup):
@@ -309,6 +309,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     pairs, cands = [], []
+    builds0 = int(sysm.graph_builds.item()) if sysm.verlet else 0
     barrier(ws)
     with ClockSampler(dev) as clk:
         for k in range(args.steps):
@@ -318,10 +319,12 @@ def run_ours(args):
             e[0].record(); pre(); e[1].record(); force(); e[2].record(); post(); e[3].record()
             torch.cuda.synchronize()
             pairs.append(sysm.pair_count())
-            cands.append(sysm.candidate_pairs())
+            cands.append(sysm.list_pairs() if sysm.verlet else sysm.candidate_pairs())
     barrier(ws)
+    builds = int(sysm.graph_builds.item()) - builds0 if sysm.verlet else None
     step_ms = [e[0].elapsed_time(e[3]) for e in ev]
     force_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    pre_ms = [e[0].elapsed_time(e[1]) for e in ev]
     tot_s = max_over_ranks(sum(step_ms) * 1e-3, ws)
     tot_pairs = sum_over_ranks(float(sum(pairs)), ws)
     value = tot_pairs / tot_s
@@ -350,7 +353,11 @@ def run_ours(args):
                    "steps_per_s": args.steps / tot_s, "pairs_per_step": statistics.mean(pairs),
                    "candidates_per_step": statistics.mean(cands),
                    "force_ms_per_step": statistics.mean(force_ms), "force_share": sum(force_ms) / sum(step_ms),
-                   "parallelism": f"dp{ws}" if ws > 1 else "single"},
+                   "pre_ms_per_step": statistics.mean(pre_ms), "pre_ms_max": max(pre_ms),
+                   "pre_ms_median": statistics.median(pre_ms),
+                   "parallelism": f"dp{ws}" if ws > 1 else "single",
+                   **({"skin": sysm.skin, "list_rebuilds_in_timed_steps": builds, "cells": list(sysm.box.cells)}
+                      if sysm.verlet else {})},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
                      "frac": achieved / peak_fp64, "traffic": traffic_bytes(),
                      "kernel": f"k_force_shell ({args.schedule} schedule)",
@@ -371,7 +378,7 @@ def e2e_run(torch, md, ref_sys, args):
     final state -- all inside the timed region."""
     n = ref_sys.n
     host = {k: v[:n].cpu().pin_memory() for k, v in ref_sys.initial.items()}
-    sysm = md.LJSystem(ref_sys.box, n, schedule=ref_sys.schedule, block=ref_sys.block)
+    sysm = md.LJSystem(ref_sys.box, n, schedule=ref_sys.schedule, block=ref_sys.block, skin=ref_sys.skin)
     sysm.load_host(host["x"], host["y"], host["z"], host["vx"], host["vy"], host["vz"], host["id"])
     for _ in range(2):
         sysm.graph_step(energy=True)
@@ -402,7 +409,9 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--schedule", default="buffered", choices=["shell", "buffered", "block", "loopex"])
+    ap.add_argument("--schedule", default="buffered",
+                    choices=["shell", "buffered", "block", "loopex", "verlet", "verlet_shell"])
+    ap.add_argument("--skin", type=float, default=0.3, help="Verlet skin (verlet schedules)")
     ap.add_argument("--block", type=lambda s: tuple(int(v) for v in s.split(",")), default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true", help="use the x-slab engine even at N=1")

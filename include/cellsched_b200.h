@@ -208,6 +208,48 @@ int cs_lj_forces(const cs_box *b, const cs_lj *p, int sched, int64_t n,
                  unsigned long long *npairs_dev, unsigned *status_dev, void *ws, size_t ws_bytes,
                  void *stream);
 
+/* Verlet neighbour lists, built from the cell list of a box
+ * whose cell edge is >= rc + skin.  The list of a home cell is a round table
+ * (lane -> home particle, round x lane -> partner j, no j twice in a round),
+ * so the force kernel keeps F_i in registers and writes each Newton-3
+ * reaction into the (cell, stencil entry) slot of j without conflicts; the
+ * colour-pass / buffered block structure of K2 is unchanged.
+ * cs_verlet_build: list from the current (wrapped, binned) positions, and
+ *   x0/y0/z0 = copy of x/y/z (reference for the displacement check, may be
+ *   NULL).  status_dev |= 2 (a cell holds > 32 particles) or 4 (> 64 rounds).
+ * cs_lj_forces_verlet: sched CS_SCHED_SHELL or CS_SCHED_BUFFERED; overwrites f.
+ * Between rebuilds positions must NOT be wrapped: cs_vv_kick_drift_track is
+ *   kick_drift without the wrap, setting flag[0] = 1 once a particle is more
+ *   than half_skin from x0; cs_wrap_positions wraps before the next rebuild. */
+size_t cs_verlet_list_bytes(const cs_box *b);
+int cs_verlet_build(const cs_box *b, const cs_lj *p, double skin, const int32_t *cell_start,
+                    const double *x, const double *y, const double *z, void *list,
+                    size_t list_bytes, double *x0, double *y0, double *z0, int64_t n,
+                    unsigned *status_dev, void *stream);
+int cs_lj_forces_verlet(const cs_box *b, const cs_lj *p, int sched, int64_t n,
+                        const int32_t *cell_start, const void *list, const double *x,
+                        const double *y, const double *z, double *fx, double *fy, double *fz,
+                        double *energy_dev, unsigned long long *npairs_dev, unsigned *status_dev,
+                        void *ws, size_t ws_bytes, void *stream);
+int cs_wrap_positions(int64_t n, const cs_box *b, double *x, double *y, double *z, void *stream);
+int cs_vv_kick_drift_track(int64_t n, double hdtm, double dt, const double *fx, const double *fy,
+                           const double *fz, double *vx, double *vy, double *vz, double *x,
+                           double *y, double *z, const double *x0, const double *y0,
+                           const double *z0, double half_skin, int32_t *flag, void *stream);
+
+/* Rebinning in place: copy the cell-sorted x, v, id back over the source. */
+int cs_copy7(int64_t n, const double *x, const double *y, const double *z, const double *vx,
+             const double *vy, const double *vz, const int32_t *id, double *xo, double *yo,
+             double *zo, double *vxo, double *vyo, double *vzo, int32_t *ido, void *stream);
+/* Device-side conditional rebuild inside a CUDA graph being captured on
+ * `stream`: appends a kernel that turns flag[0] into the condition of an IF
+ * node (and clears the flag), appends the IF node, and starts capturing its
+ * body on `side_stream`; launch the rebuild work on side_stream, then call
+ * cs_capture_if_end(side_stream).  Capture continues on `stream` after the
+ * IF node. */
+int cs_capture_if_begin(void *stream, void *side_stream, int32_t *flag, int32_t *count);
+int cs_capture_if_end(void *side_stream);
+
 /* K3: velocity Verlet.  kick: v += (dt/2m) f.  kick_drift: v += (dt/2m) f;
  * x += dt v; wrap into [0, L) on periodic axes. */
 int cs_vv_kick(int64_t n, double hdtm, const double *fx, const double *fy, const double *fz,

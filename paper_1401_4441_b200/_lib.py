@@ -85,6 +85,14 @@ _SIGS = {
     "cs_vv_kick_drift": (C.c_int, [_I64, _D, _D, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "cs_kinetic": (C.c_int, [_I64, _D, _P, _P, _P, _P, _P, _SZ, _P]),
     "cs_sum3": (C.c_int, [_I64, _P, _P, _P, _P, _P, _SZ, _P]),
+    "cs_verlet_list_bytes": (_SZ, [_P]),
+    "cs_verlet_build": (C.c_int, [_P, _P, _D, _P, _P, _P, _P, _P, _SZ, _P, _P, _P, _I64, _P, _P]),
+    "cs_lj_forces_verlet": (C.c_int, [_P, _P, C.c_int, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "cs_wrap_positions": (C.c_int, [_I64, _P, _P, _P, _P, _P]),
+    "cs_vv_kick_drift_track": (C.c_int, [_I64, _D, _D] + [_P] * 12 + [_D, _P, _P]),
+    "cs_copy7": (C.c_int, [_I64] + [_P] * 15),
+    "cs_capture_if_begin": (C.c_int, [_P, _P, _P, _P]),
+    "cs_capture_if_end": (C.c_int, [_P]),
     "cs_pack_plane": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _D, _P, _P]),
     "cs_add_plane_forces": (C.c_int, [_P, C.c_int, _P, _P, _P, _P, _P, _P]),
     "cs_probe_dfma": (C.c_int, [C.c_int, C.c_int, _P, _P]),

@@ -36,6 +36,10 @@ struct ForceArgs {
   unsigned *hits_cell;
   int nbk[3];  // blocks per axis (block schedule)
   int cap;     // shared-memory particle capacity (block schedule)
+  // Verlet round tables (cs_verlet.cuh); null for the link-cell schedules
+  const int32_t *vl_nround;
+  const uint8_t *vl_imap;
+  const uint16_t *vl_desc;
 };
 
 // level (0..26) -> (stencil entry, parity); level 0 = intra
@@ -362,17 +366,35 @@ static int check_lj_box(const Box &b, double rc) {
   return CS_OK;
 }
 
-static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, cs_ws *w,
-                               int64_t n, unsigned *status, cudaStream_t st);
+static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, bool verlet,
+                               cs_ws *w, int64_t n, unsigned *status, cudaStream_t st);
+
+// vlist: Verlet round tables (cs_verlet.cuh) or null for the link-cell path
+static int lj_forces_impl(const cs_box *bx, const cs_lj *lj, int sched, int64_t npart,
+                          const int32_t *cell_start, const void *vlist, const double *x,
+                          const double *y, const double *z, double *fx, double *fy, double *fz,
+                          double *energy_dev, unsigned long long *npairs_dev,
+                          unsigned *status_dev, void *ws, size_t ws_bytes, cudaStream_t st);
 
 extern "C" int cs_lj_forces(const cs_box *bx, const cs_lj *lj, int sched, int64_t npart,
                             const int32_t *cell_start, const double *x, const double *y,
                             const double *z, double *fx, double *fy, double *fz,
                             double *energy_dev, unsigned long long *npairs_dev,
                             unsigned *status_dev, void *ws, size_t ws_bytes, void *stream) {
+  return lj_forces_impl(bx, lj, sched, npart, cell_start, nullptr, x, y, z, fx, fy, fz,
+                        energy_dev, npairs_dev, status_dev, ws, ws_bytes, cs_stream(stream));
+}
+
+static void vl_attach(ForceArgs &A, const void *vlist);  // cs_verlet.cuh
+
+static int lj_forces_impl(const cs_box *bx, const cs_lj *lj, int sched, int64_t npart,
+                          const int32_t *cell_start, const void *vlist, const double *x,
+                          const double *y, const double *z, double *fx, double *fy, double *fz,
+                          double *energy_dev, unsigned long long *npairs_dev,
+                          unsigned *status_dev, void *ws, size_t ws_bytes, cudaStream_t st) {
   CS_TRY(cs_upload_stencil());
-  cudaStream_t st = cs_stream(stream);
   ForceArgs A;
+  memset(&A, 0, sizeof(A));
   CS_TRY(make_box(bx, &A.b));
   CS_TRY(check_lj_box(A.b, lj->rc));
   A.p.rc2 = lj->rc * lj->rc;
@@ -397,7 +419,18 @@ extern "C" int cs_lj_forces(const cs_box *bx, const cs_lj *lj, int sched, int64_
   const bool energy = energy_dev != nullptr;
   if (energy) CS_CUDA(cudaMemsetAsync(pe_cell, 0, sizeof(double) * nc, st));
   CS_CUDA(cudaMemsetAsync(hits_cell, 0, sizeof(unsigned) * nc, st));
-  if (sched == CS_SCHED_LOOPEX) {
+  if (vlist) {
+    CS_REQUIRE(sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED,
+               "Verlet forces run under CS_SCHED_SHELL or CS_SCHED_BUFFERED");
+    vl_attach(A, vlist);
+    CS_TRY(block_grid(A.b, A.nbk));
+    if (sched == CS_SCHED_SHELL) {  // in-place colour passes accumulate: start from zero
+      CS_CUDA(cudaMemsetAsync(fx, 0, sizeof(double) * npart, st));
+      CS_CUDA(cudaMemsetAsync(fy, 0, sizeof(double) * npart, st));
+      CS_CUDA(cudaMemsetAsync(fz, 0, sizeof(double) * npart, st));
+    }
+    CS_TRY(launch_shell_passes(A, energy, sched == CS_SCHED_BUFFERED, true, &w, npart, status_dev, st));
+  } else if (sched == CS_SCHED_LOOPEX) {
     for (int level = 0; level < 27; ++level) {
       int64_t ntask = (int64_t)A.b.owned_x * A.b.nc[1] * A.b.nc[2];  // upper bound
       if (level > 0) ntask = (ntask + 1) / 2 + (int64_t)A.b.nc[1] * A.b.nc[2];
@@ -431,7 +464,7 @@ extern "C" int cs_lj_forces(const cs_box *bx, const cs_lj *lj, int sched, int64_
     }
   } else if (sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED) {
     CS_TRY(block_grid(A.b, A.nbk));
-    CS_TRY(launch_shell_passes(A, energy, sched == CS_SCHED_BUFFERED, &w, npart, status_dev, st));
+    CS_TRY(launch_shell_passes(A, energy, sched == CS_SCHED_BUFFERED, false, &w, npart, status_dev, st));
   } else {
     CS_REQUIRE(0, "unknown schedule %d", sched);
   }

@@ -26,18 +26,23 @@
 //
 // No atomics on forces, no intra-CTA dependency levels, deterministic order.
 #pragma once
+#include <type_traits>
+
 #include "cs_force.cuh"
 
 #define SH_NW 8        // warps per CTA (one home cell each for 2x2x2 blocks)
-#define SH_IB 16       // home particles per row block (= i-owner lanes)
-#define SH_FB 128      // hit window: forces staged per warp
-#define SH_DCAP 512    // hit descriptors per chunk (32 j x 16 i)
+#define SH_IB 4        // home particles per filter row block
 #define SH_JCAP 384    // j list capacity per warp (>= particles of the 14 source cells)
 #define SH_RCAP 1440   // reaction slots (particles) per CTA
 #define SH_HCAP 160    // home particles per CTA
 #define SH_MAXB 8      // home cells per CTA
 #define SH_MAXF 64     // footprint cells per CTA ((Bx+1)(By+2)(Bz+2))
 #define SH_MAXC 8      // contributors per footprint cell
+// Verlet mode (cells of edge >= rc + skin, ~20 particles per cell)
+#define VL_RCAP 2560   // reaction slots per CTA
+#define VL_HCAP 256    // home particles per CTA
+#define VL_RMAX 64     // rounds per home cell in the round tables
+#define VL_IDLE 0x0F00u  // idle slot descriptor (entry 15, index 0)
 
 struct MergeTable {              // host-built per block shape
   uint8_t n[SH_MAXF];            // contributors of footprint cell lc
@@ -45,25 +50,26 @@ struct MergeTable {              // host-built per block shape
   int nfc;
 };
 
-struct ShellSmem {
-  double R[3][SH_RCAP];              // reaction slots (e >= 1)
-  double Fh[3][SH_HCAP];             // home rows (e = 0)
-  double hxd[SH_NW][SH_IB][4];       // home positions (fp64, exact re-test)
-  float4 hxf[SH_NW][SH_IB];          // home positions relative to the cell (fp32 filter)
-  double fb[SH_NW][3][SH_FB];        // forces of the current hit window
-  uint16_t desc[SH_NW][SH_DCAP];     // hit descriptors (j lane << 5 | i), j-major
-  int seg[SH_NW][32];                // lane j: first descriptor of its hits
-  unsigned msk[SH_NW][32];           // lane j: hit mask over the row block
-  double sh[SH_MAXB][14][3];         // image shift of source (h, e)
-  uint16_t jl[SH_NW][SH_JCAP];       // j list: entry << 12 | index in source cell
-  int sstart[SH_MAXB][14];           // global start of source (h, e)
-  int scount[SH_MAXB][14];           // count of source (h, e), -1: none
-  int sbase[SH_MAXB][14];            // slot base (Fh for e = 0, R for e >= 1)
+template <int RCAP_, int HCAP_>
+struct ShellBase {
+  static constexpr int RCAP = RCAP_, HCAP = HCAP_;
+  double R[3][RCAP];                 // reaction slots (e >= 1)
+  double Fh[3][HCAP];                // home rows (e = 0)
+  double sh[SH_MAXB][16][3];         // image shift of source (h, e); e = 15: idle
+  int sstart[SH_MAXB][16];           // global start of source (h, e)
+  int scount[SH_MAXB][16];           // count of source (h, e), -1: none
+  int sbase[SH_MAXB][16];            // slot base (Fh for e = 0, R for e >= 1)
   int fstart[SH_MAXF + 1];           // footprint cell -> offset in the block buffer
   int fgstart[SH_MAXF];              // footprint cell -> global start (-1: none)
   int hcell[SH_MAXB];
   int overflow;
 };
+struct ShellSmem : ShellBase<SH_RCAP, SH_HCAP> {  // link-cell super-tasks
+  double rows[SH_NW][SH_IB][3][32];  // per-lane i partials
+  double hx[SH_NW][SH_IB][4];        // broadcast home positions
+  uint16_t jl[SH_NW][SH_JCAP];       // j list: entry << 12 | index in source cell
+};
+struct ShellSmemVL : ShellBase<VL_RCAP, VL_HCAP> {};  // Verlet round tables
 
 __device__ __forceinline__ double box_d2(double x, double lo, double hi) {
   const double d = fmax(fmax(lo - x, 0.0), x - hi);
@@ -82,6 +88,149 @@ __device__ __forceinline__ double fast_rcp(double a) {
 
 __device__ __forceinline__ int wrap1i(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
 
+// Verlet mode, steps 1-4 for every home cell of this warp.  The round table
+// of home cell h (cs_verlet.cuh) gives every lane a first home particle and
+// possibly a second one from a switch round on; per round a lane has at most
+// one partner j (stencil entry << 8 | index in the source cell) and no j
+// appears twice in a round.  So F_i stays in registers, and the reaction on
+// j is a read-modify-write of its (h, e) slot that no other lane touches in
+// that round (no atomics).  Every listed pair is re-tested exactly
+// (r^2 < rc^2).  Descriptors are prefetched two rounds ahead and partner
+// positions one round ahead (the image shift is added when used).
+template <bool ENERGY, class SM>
+__device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, int a0,
+                                             const uint16_t *dp, int nr, int pA, int pB, int sw,
+                                             double *fa, double *fb, double &pe,
+                                             unsigned &hits) {
+  constexpr int RCAP = SM::RCAP, HCAP = SM::HCAP;
+  const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
+  double xi = 0, yi = 0, zi = 0, xb = 0, yb = 0, zb = 0;
+  if (pA != 0xFF) {
+    xi = __ldg(A.x + a0 + pA);
+    yi = __ldg(A.y + a0 + pA);
+    zi = __ldg(A.z + a0 + pA);
+  }
+  if (pB != 0xFF) {
+    xb = __ldg(A.x + a0 + pB);
+    yb = __ldg(A.y + a0 + pB);
+    zb = __ldg(A.z + a0 + pB);
+  }
+  double fx_ = 0, fy_ = 0, fz_ = 0;
+  // idle slots are entry 15: a real particle shifted 1e150 away (no branch)
+  unsigned d0 = nr > 0 ? __ldg(dp) : VL_IDLE;
+  unsigned d1 = nr > 1 ? __ldg(dp + 32) : VL_IDLE;
+  int g0 = S.sstart[h][d0 >> 8] + (d0 & 255);
+  double x0 = __ldg(A.x + g0), y0 = __ldg(A.y + g0), z0 = __ldg(A.z + g0);
+  dp += 64;
+  for (int r = 0; r < nr; ++r) {
+    if (r == sw) {  // this lane continues with its second particle
+      fa[0] = fx_;
+      fa[1] = fy_;
+      fa[2] = fz_;
+      fx_ = fy_ = fz_ = 0;
+      xi = xb;
+      yi = yb;
+      zi = zb;
+    }
+    const unsigned d2 = r + 2 < nr ? __ldg(dp) : VL_IDLE;
+    dp += 32;
+    const int g1 = S.sstart[h][d1 >> 8] + (d1 & 255);
+    const double x1 = __ldg(A.x + g1), y1 = __ldg(A.y + g1), z1 = __ldg(A.z + g1);
+    {
+      const int e = d0 >> 8;
+      const double dx = xi - (x0 + S.sh[h][e][0]), dy = yi - (y0 + S.sh[h][e][1]),
+                   dz = zi - (z0 + S.sh[h][e][2]);
+      const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+      if (r2 < rc2) {
+        const double ri = fast_rcp(r2);
+        const double s2 = sig2 * ri;
+        const double s6 = s2 * s2 * s2;
+        const double ff = eps48 * s6 * (s6 - 0.5) * ri;
+        const double fx = ff * dx, fy = ff * dy, fz = ff * dz;
+        fx_ += fx;
+        fy_ += fy;
+        fz_ += fz;
+        const int slot = S.sbase[h][e] + (d0 & 255);
+        double *dst = e == 0 ? &S.Fh[0][slot] : &S.R[0][slot];
+        const int stride = e == 0 ? HCAP : RCAP;
+        dst[0] -= fx;
+        dst[stride] -= fy;
+        dst[2 * stride] -= fz;
+        if (ENERGY) pe += eps4 * s6 * (s6 - 1.0);
+        ++hits;
+      }
+    }
+    d0 = d1;
+    d1 = d2;
+    x0 = x1;
+    y0 = y1;
+    z0 = z1;
+    __syncwarp();
+  }
+  if (sw < nr) {
+    fb[0] = fx_;
+    fb[1] = fy_;
+    fb[2] = fz_;
+  } else {
+    fa[0] = fx_;
+    fa[1] = fy_;
+    fa[2] = fz_;
+  }
+}
+
+// lanes of one home particle are contiguous: segmented reduction, then the
+// first lane of each run adds the particle's F_i into its home row
+template <class SM>
+__device__ __forceinline__ void verlet_fi(SM &S, int h, int lane, int im, double fix, double fiy,
+                                          double fiz) {
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const double ux = __shfl_down_sync(CS_FULL, fix, s);
+    const double uy = __shfl_down_sync(CS_FULL, fiy, s);
+    const double uz = __shfl_down_sync(CS_FULL, fiz, s);
+    const int ui = __shfl_down_sync(CS_FULL, im, s);
+    if (lane + s < 32 && ui == im) {
+      fix += ux;
+      fiy += uy;
+      fiz += uz;
+    }
+  }
+  const int prev = __shfl_up_sync(CS_FULL, im, 1);
+  if (im != 0xFF && (lane == 0 || prev != im)) {
+    const int slot = S.sbase[h][0] + im;
+    S.Fh[0][slot] += fix;
+    S.Fh[1][slot] += fiy;
+    S.Fh[2][slot] += fiz;
+  }
+  __syncwarp();
+}
+
+template <bool ENERGY, class SM>
+__device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lane, int wid,
+                                              int nhome) {
+  for (int h = wid; h < nhome; h += SH_NW) {
+    const int cell = S.hcell[h];
+    if (cell < 0) continue;
+    const uint8_t *lm = A.vl_imap + (int64_t)cell * 96;
+    const int nr = A.vl_nround[cell];
+    const int pA = lm[lane], pB = lm[32 + lane], sw = lm[64 + lane];
+    double pe = 0;
+    unsigned hits = 0;
+    double fa[3] = {0, 0, 0}, fb[3] = {0, 0, 0};
+    verlet_table<ENERGY>(S, A, h, S.sstart[h][0], A.vl_desc + (int64_t)cell * (VL_RMAX * 32) + lane,
+                         nr, pA, pB, sw, fa, fb, pe, hits);
+    verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2]);
+    verlet_fi(S, h, lane, pB, fb[0], fb[1], fb[2]);
+    hits = warp_sum(hits);
+    if (ENERGY) pe = warp_sum(pe);
+    if (lane == 0) {
+      A.hits_cell[cell] += hits;
+      if (ENERGY) A.pe_cell[cell] += pe;
+    }
+    __syncwarp();
+  }
+}
+
 struct ShellArgs {
   ForceArgs A;
   MergeTable mt;
@@ -90,6 +239,7 @@ struct ShellArgs {
   int *bindex;            // buffered mode: per block fstart[0..SH_MAXF]
   int64_t bufstride;
   unsigned *err;          // capacity overflow flag (buffered mode)
+  int overwrite;          // buffered gather stores instead of adding (Verlet mode)
 };
 
 // block coordinates -> global cell of a footprint cell (or -1)
@@ -101,10 +251,12 @@ __device__ __forceinline__ int64_t foot_cell(const Box &b, const int *o0, int lc
   return box_cell(b, v0, v1, v2);
 }
 
-template <bool ENERGY, bool BUFFERED>
-__global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int colour) {
+template <bool ENERGY, bool BUFFERED, bool VERLET>
+__global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int colour) {
   extern __shared__ __align__(16) unsigned char sh_raw[];
-  ShellSmem &S = *reinterpret_cast<ShellSmem *>(sh_raw);
+  using SM = typename std::conditional<VERLET, ShellSmemVL, ShellSmem>::type;
+  constexpr int RCAP = SM::RCAP, HCAP = SM::HCAP;
+  SM &S = *reinterpret_cast<SM *>(sh_raw);
   const ForceArgs &A = SA.A;
   const Box &b = A.b;
   const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
@@ -154,6 +306,11 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
     S.sh[h][e][0] = s0;
     S.sh[h][e][1] = s1;
     S.sh[h][e][2] = s2;
+    if (e == 0) {  // Verlet idle slots: entry 15 reads a real particle at 1e150 away
+      S.sstart[h][15] = st;
+      S.sbase[h][15] = 0;
+      S.sh[h][15][0] = S.sh[h][15][1] = S.sh[h][15][2] = 1e150;
+    }
   }
   for (int lc = threadIdx.x; lc < nfc; lc += blockDim.x) {
     const int64_t gc = foot_cell(b, o0, lc, FX, FY);
@@ -199,15 +356,15 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
     }
     if (lane == 0) {
       S.fstart[0] = 0;
-      S.overflow = (fb > SH_HCAP || rb > SH_RCAP || src_max > SH_JCAP) ? 1 : 0;
+      S.overflow = (fb > HCAP || rb > RCAP || (!VERLET && src_max > SH_JCAP)) ? 1 : 0;
     }
   }
   __syncthreads();
   if (S.overflow) {
-    if (BUFFERED) {  // no in-place fallback in buffered mode: report to the host
+    if constexpr (BUFFERED) {  // no in-place fallback in buffered mode: report to the host
       if (threadIdx.x == 0) atomicExch(SA.err, 1u);
       return;
-    }
+    } else {
     // colour mode fallback: v1 per-task routine on global memory under the 27
     // loop-exchange levels inside this block (still conflict-free)
     for (int level = 0; level < 27; ++level) {
@@ -230,24 +387,27 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
       __syncthreads();
     }
     return;
+    }
   }
-  for (int i = threadIdx.x; i < SH_RCAP; i += blockDim.x) S.R[0][i] = S.R[1][i] = S.R[2][i] = 0.0;
-  for (int i = threadIdx.x; i < SH_HCAP; i += blockDim.x) S.Fh[0][i] = S.Fh[1][i] = S.Fh[2][i] = 0.0;
+  for (int i = threadIdx.x; i < RCAP; i += blockDim.x) S.R[0][i] = S.R[1][i] = S.R[2][i] = 0.0;
+  for (int i = threadIdx.x; i < HCAP; i += blockDim.x) S.Fh[0][i] = S.Fh[1][i] = S.Fh[2][i] = 0.0;
   __syncthreads();
 
   const double edge0 = b.L[0] / b.gnc[0], edge1 = b.L[1] / b.gnc[1], edge2 = b.L[2] / b.gnc[2];
   const double cull2 = A.p.rc2 * (1.0 + 1e-12) + 1e-12;
   const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
-  const float rc2f = (float)(rc2 + 1e-3);  // conservative fp32 prefilter bound (exact fp64 re-test)
   // ---- 1-4. one warp per home cell
+  if constexpr (VERLET) {
+    verlet_rounds<ENERGY>(S, A, lane, wid, nhome);
+  } else {
   for (int h = wid; h < nhome; h += SH_NW) {
     if (S.hcell[h] < 0) continue;
     const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
     const int a0 = S.sstart[h][0], na = S.scount[h][0];
-    const double lo0 = (b.x0 + hg0) * edge0, lo1 = hg1 * edge1, lo2 = hg2 * edge2;
-    (void)cull2;
-    // 1. j list = the 14 source cells concatenated (home first); lanes walk
-    //    the concatenation directly
+    (void)hg0; (void)hg1; (void)hg2; (void)cull2; (void)edge0; (void)edge1; (void)edge2;
+    // 1. j list = the 14 source cells concatenated (home first).  Lanes walk
+    //    the concatenation directly (no per-cell partial warps); a box-distance
+    //    cull was measured to cost more than the candidates it removes.
     const int mycnt = lane < 14 ? max(S.scount[h][lane], 0) : 0;
     int incl = mycnt;
 #pragma unroll
@@ -277,15 +437,15 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
       const int nib = min(SH_IB, na - ib);
       if (lane < SH_IB) {
         const int ii = a0 + ib + min(lane, nib - 1);
-        const double x = __ldg(A.x + ii), y = __ldg(A.y + ii), z = __ldg(A.z + ii);
-        S.hxd[wid][lane][0] = x;
-        S.hxd[wid][lane][1] = y;
-        S.hxd[wid][lane][2] = z;
-        S.hxf[wid][lane] = make_float4((float)(x - lo0), (float)(y - lo1), (float)(z - lo2), 0.f);
+        S.hx[wid][lane][0] = __ldg(A.x + ii);
+        S.hx[wid][lane][1] = __ldg(A.y + ii);
+        S.hx[wid][lane][2] = __ldg(A.z + ii);
       }
+#pragma unroll
+      for (int q = 0; q < SH_IB; ++q)
+        S.rows[wid][q][0][lane] = S.rows[wid][q][1][lane] = S.rows[wid][q][2][lane] = 0.0;
       __syncwarp();
       const unsigned qmask = (1u << nib) - 1;
-      double fix = 0, fiy = 0, fiz = 0;  // F_i of i-owner lane (i = ib + lane, lane < nib)
       for (int c0 = 0; c0 < nj; c0 += 32) {
         const int jj = c0 + lane;
         const bool vj = jj < nj;
@@ -298,114 +458,84 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
           yj = __ldg(A.y + gj) + S.sh[h][e][1];
           zj = __ldg(A.z + gj) + S.sh[h][e][2];
         }
-        // 2. fp32 prefilter: 16 rows against this lane's j
-        const float xf = (float)(xj - lo0), yf = (float)(yj - lo1), zf = (float)(zj - lo2);
-        unsigned m = 0;
+        // intra (e == 0): only pairs i < j, i.e. rows qq < q - ib
+        const int jr = (vj && e == 0) ? q - ib : SH_IB + 1;
+        unsigned mask = 0;
 #pragma unroll
         for (int qq = 0; qq < SH_IB; ++qq) {
-          const float4 p = S.hxf[wid][qq];
-          const float dx = p.x - xf, dy = p.y - yf, dz = p.z - zf;
-          m |= (unsigned)(__fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx)) < rc2f) << qq;
+          const double dx = S.hx[wid][qq][0] - xj, dy = S.hx[wid][qq][1] - yj,
+                       dz = S.hx[wid][qq][2] - zj;
+          const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+          mask |= (unsigned)(r2 < rc2 && qq < jr) << qq;
         }
-        if (e == 0) m &= (q - ib <= 0) ? 0u : (q - ib >= SH_IB ? 0xFFFFu : ((1u << (q - ib)) - 1));
-        m = vj ? (m & qmask) : 0u;
-        // 3. j-major compaction of the hits into descriptors
-        const int cnt = __popc(m);
-        int ci = cnt;
-#pragma unroll
-        for (int s = 1; s < 32; s <<= 1) {
-          const int v = __shfl_up_sync(CS_FULL, ci, s);
-          if (lane >= s) ci += v;
-        }
-        const int seg = ci - cnt;
-        const int T = __shfl_sync(CS_FULL, ci, 31);
-        if (T == 0) continue;
-        S.seg[wid][lane] = seg;
-        S.msk[wid][lane] = m;
-        {
-          unsigned mm = m;
-          int r = seg;
-          while (mm) {
-            const int qq = __ffs(mm) - 1;
-            mm &= mm - 1;
-            S.desc[wid][r++] = (uint16_t)((lane << 5) | qq);
-          }
-        }
-        // transposed rows: bit jl of rowm = hit (i = lane, j = lane jl)
-        unsigned rowm = 0;
-#pragma unroll
-        for (int qq = 0; qq < SH_IB; ++qq) {
-          const unsigned bq = __ballot_sync(CS_FULL, (m >> qq) & 1u);
-          if (lane == qq) rowm = bq;
-        }
-        __syncwarp();
-        double gx = 0, gy = 0, gz = 0;  // reaction on this lane's j
-        for (int w0 = 0; w0 < T; w0 += SH_FB) {  // hit windows (one in practice)
-          const int wn = min(SH_FB, T - w0);
-          for (int t0 = 0; t0 < wn; t0 += 32) {  // dense rounds: every lane one hit
-            const int t = t0 + lane;
-            const bool act = t < wn;
-            const int d = act ? S.desc[wid][w0 + t] : 0;
-            const int jl = d >> 5, qq = d & 31;
-            const double xjl = __shfl_sync(CS_FULL, xj, jl), yjl = __shfl_sync(CS_FULL, yj, jl),
-                         zjl = __shfl_sync(CS_FULL, zj, jl);
-            double fx = 0, fy = 0, fz = 0;
-            if (act) {
-              const double dx = S.hxd[wid][qq][0] - xjl, dy = S.hxd[wid][qq][1] - yjl,
-                           dz = S.hxd[wid][qq][2] - zjl;
-              const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
-              if (r2 < rc2) {  // exact test (same expression as the oracle)
-                const double rinv2 = fast_rcp(r2);
-                const double sr2 = sig2 * rinv2;
-                const double sr6 = sr2 * sr2 * sr2;
-                const double ff = eps48 * sr6 * (sr6 - 0.5) * rinv2;
-                fx = ff * dx;
-                fy = ff * dy;
-                fz = ff * dz;
-                if (ENERGY) pe += eps4 * sr6 * (sr6 - 1.0);
-                ++hits;
-              }
-              S.fb[wid][0][t] = fx;
-              S.fb[wid][1][t] = fy;
-              S.fb[wid][2][t] = fz;
+        mask &= qmask;
+        double gx = 0, gy = 0, gz = 0;
+        // two hits per lane per step: independent dependency chains (ILP);
+        // both write different rows of this lane's private partials
+        while (__any_sync(CS_FULL, mask)) {
+          const bool h1 = mask != 0;
+          const int q1 = h1 ? __ffs(mask) - 1 : 0;
+          mask &= mask - 1;
+          const bool h2 = mask != 0;
+          const int q2 = h2 ? __ffs(mask) - 1 : 0;
+          mask &= mask - 1;
+          if (h1) {
+            const double dx1 = S.hx[wid][q1][0] - xj, dy1 = S.hx[wid][q1][1] - yj,
+                         dz1 = S.hx[wid][q1][2] - zj;
+            const double dx2 = S.hx[wid][q2][0] - xj, dy2 = S.hx[wid][q2][1] - yj,
+                         dz2 = S.hx[wid][q2][2] - zj;
+            const double r21 = __fma_rn(dz1, dz1, __fma_rn(dy1, dy1, dx1 * dx1));
+            const double r22 = h2 ? __fma_rn(dz2, dz2, __fma_rn(dy2, dy2, dx2 * dx2)) : 1.0;
+            const double ri1 = fast_rcp(r21), ri2 = fast_rcp(r22);
+            const double s21 = sig2 * ri1, s22 = sig2 * ri2;
+            const double s61 = s21 * s21 * s21, s62 = s22 * s22 * s22;
+            const double ff1 = eps48 * s61 * (s61 - 0.5) * ri1;
+            const double ff2 = h2 ? eps48 * s62 * (s62 - 0.5) * ri2 : 0.0;
+            const double fx1 = ff1 * dx1, fy1 = ff1 * dy1, fz1 = ff1 * dz1;
+            const double fx2 = ff2 * dx2, fy2 = ff2 * dy2, fz2 = ff2 * dz2;
+            gx -= fx1;
+            gy -= fy1;
+            gz -= fz1;
+            S.rows[wid][q1][0][lane] += fx1;
+            S.rows[wid][q1][1][lane] += fy1;
+            S.rows[wid][q1][2][lane] += fz1;
+            if (ENERGY) pe += eps4 * s61 * (s61 - 1.0);
+            ++hits;
+            if (h2) {
+              gx -= fx2;
+              gy -= fy2;
+              gz -= fz2;
+              S.rows[wid][q2][0][lane] += fx2;
+              S.rows[wid][q2][1][lane] += fy2;
+              S.rows[wid][q2][2][lane] += fz2;
+              if (ENERGY) pe += eps4 * s62 * (s62 - 1.0);
+              ++hits;
             }
           }
-          __syncwarp();
-          // F_j: this lane's hits are the contiguous descriptors [seg, seg+cnt)
-          const int lo = max(seg, w0), hi = min(seg + cnt, w0 + wn);
-          for (int t = lo; t < hi; ++t) {
-            gx -= S.fb[wid][0][t - w0];
-            gy -= S.fb[wid][1][t - w0];
-            gz -= S.fb[wid][2][t - w0];
-          }
-          // F_i: i-owner lanes walk their row bits
-          if (lane < nib) {
-            for (unsigned mm = rowm; mm; mm &= mm - 1) {
-              const int jl = __ffs(mm) - 1;
-              const int pos = S.seg[wid][jl] + __popc(S.msk[wid][jl] & ((1u << lane) - 1)) - w0;
-              if (pos >= 0 && pos < wn) {
-                fix += S.fb[wid][0][pos];
-                fiy += S.fb[wid][1][pos];
-                fiz += S.fb[wid][2][pos];
-              }
-            }
-          }
-          __syncwarp();
         }
-        if (cnt) {  // unique writer of slot (h, e, q)
+        if (vj) {  // unique writer of slot (h, e, q)
           const int slot = S.sbase[h][e] + q;
           double *dst = e == 0 ? &S.Fh[0][slot] : &S.R[0][slot];
-          const int stride = e == 0 ? SH_HCAP : SH_RCAP;
+          const int stride = e == 0 ? HCAP : RCAP;
           dst[0] += gx;
           dst[stride] += gy;
           dst[2 * stride] += gz;
         }
-        __syncwarp();
       }
-      if (lane < nib) {  // own row (after this row block's intra reactions)
-        S.Fh[0][fh0 + ib + lane] += fix;
-        S.Fh[1][fh0 + ib + lane] += fiy;
-        S.Fh[2][fh0 + ib + lane] += fiz;
+      __syncwarp();
+      if (lane < 3 * SH_IB) {  // lane (q, c) reduces row q component c
+        const int q = lane / 3, c = lane - 3 * (lane / 3);
+        if (q < nib) {
+          double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+          for (int l = 0; l < 32; l += 4) {
+            s0 += S.rows[wid][q][c][l];
+            s1 += S.rows[wid][q][c][l + 1];
+            s2 += S.rows[wid][q][c][l + 2];
+            s3 += S.rows[wid][q][c][l + 3];
+          }
+          S.Fh[c][fh0 + ib + q] += (s0 + s1) + (s2 + s3);
+        }
       }
       __syncwarp();
     }
@@ -416,6 +546,7 @@ __global__ void __launch_bounds__(SH_NW * 32, 2) k_force_shell(ShellArgs SA, int
       if (ENERGY) A.pe_cell[S.hcell[h]] += pe;
     }
   }
+  }  // link-cell super-tasks
   __syncthreads();
   // ---- 5. merge per footprint cell in a fixed order
   const int64_t boff = BUFFERED ? SA.boff[bid] : 0;
@@ -532,9 +663,15 @@ __global__ void k_gather_blocks(ShellArgs SA) {
       }
     }
     if (i < n) {
-      A.fx[g0 + i] += sx;
-      A.fy[g0 + i] += sy;
-      A.fz[g0 + i] += sz;
+      if (SA.overwrite) {
+        A.fx[g0 + i] = sx;
+        A.fy[g0 + i] = sy;
+        A.fz[g0 + i] = sz;
+      } else {
+        A.fx[g0 + i] += sx;
+        A.fy[g0 + i] += sy;
+        A.fz[g0 + i] += sz;
+      }
     }
   }
 }
@@ -570,23 +707,36 @@ static size_t shell_buffered_ws(const Box &b, int64_t n) {
          cs_ws_slice(sizeof(int32_t) * nb * (SH_MAXF + 1)) + cs_scan_ws_bytes(nb) + cs_ws_slice(64);
 }
 
-static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, cs_ws *w,
-                               int64_t n, unsigned *status, cudaStream_t st) {
+typedef void (*ShellKernel)(ShellArgs, int);
+static ShellKernel shell_kernel(bool energy, bool buffered, bool verlet) {
+  static const ShellKernel k[8] = {
+      k_force_shell<false, false, false>, k_force_shell<true, false, false>,
+      k_force_shell<false, true, false>,  k_force_shell<true, true, false>,
+      k_force_shell<false, false, true>,  k_force_shell<true, false, true>,
+      k_force_shell<false, true, true>,   k_force_shell<true, true, true>};
+  return k[(verlet ? 4 : 0) + (buffered ? 2 : 0) + (energy ? 1 : 0)];
+}
+
+static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, bool verlet,
+                               cs_ws *w, int64_t n, unsigned *status, cudaStream_t st) {
   const int B[3] = {A.b.blk[0], A.b.blk[1], A.b.blk[2]};
   CS_REQUIRE(B[0] * B[1] * B[2] <= SH_MAXB, "shell schedule: block has more than %d cells", SH_MAXB);
   ShellArgs SA;
   memset(&SA, 0, sizeof(SA));
   SA.A = A;
+  SA.overwrite = verlet ? 1 : 0;
   CS_TRY(build_merge_table(B, &SA.mt));
-  const size_t smem = sizeof(ShellSmem);
+  const size_t smem = verlet ? sizeof(ShellSmemVL) : sizeof(ShellSmem);
   static bool attr = false;
   if (!attr) {
-    CS_CUDA(cudaFuncSetAttribute(k_force_shell<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CS_CUDA(cudaFuncSetAttribute(k_force_shell<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CS_CUDA(cudaFuncSetAttribute(k_force_shell<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CS_CUDA(cudaFuncSetAttribute(k_force_shell<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (int v = 0; v < 8; ++v) {
+      const size_t sm = (v & 4) ? sizeof(ShellSmemVL) : sizeof(ShellSmem);
+      CS_CUDA(cudaFuncSetAttribute(shell_kernel(v & 1, v & 2, v & 4),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
     attr = true;
   }
+  const ShellKernel kern = shell_kernel(energy, buffered, verlet);
   if (buffered) {
     const int64_t nblocks = (int64_t)A.nbk[0] * A.nbk[1] * A.nbk[2];
     CS_WS_TAKE(*w, double, buf, 3 * (8 * n + 64));
@@ -604,10 +754,7 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, c
     SA.err = status ? status : err;
     k_block_sizes<<<grid_for(nblocks * 32, 256), 256, 0, st>>>(SA, sizes);
     CS_TRY(cs_exclusive_scan_i32(sizes, boff, nblocks, scratch, sb, st));
-    if (energy)
-      k_force_shell<true, true><<<(unsigned)nblocks, SH_NW * 32, smem, st>>>(SA, -1);
-    else
-      k_force_shell<false, true><<<(unsigned)nblocks, SH_NW * 32, smem, st>>>(SA, -1);
+    kern<<<(unsigned)nblocks, SH_NW * 32, smem, st>>>(SA, -1);
     const int64_t ncell = (int64_t)A.b.nc[0] * A.b.nc[1] * A.b.nc[2];
     k_gather_blocks<<<(unsigned)((ncell * 32 + 255) / 256), 256, 0, st>>>(SA);
     return cs_check_launch("force_buffered");
@@ -617,10 +764,7 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, c
     unsigned blocks = 1;
     for (int k = 0; k < 3; ++k) blocks *= (unsigned)((A.nbk[k] - kc[k] + 1) >> 1);
     if (!blocks) continue;
-    if (energy)
-      k_force_shell<true, false><<<blocks, SH_NW * 32, smem, st>>>(SA, colour);
-    else
-      k_force_shell<false, false><<<blocks, SH_NW * 32, smem, st>>>(SA, colour);
+    kern<<<blocks, SH_NW * 32, smem, st>>>(SA, colour);
   }
   return cs_check_launch("force_shell");
 }

@@ -9,4 +9,5 @@
 #include "cs_md.cuh"
 #include "cs_force.cuh"
 #include "cs_force2.cuh"
+#include "cs_verlet.cuh"
 #include "cs_probe.cuh"

@@ -1,0 +1,530 @@
+// cs_verlet.cuh -- Verlet neighbour lists for the K2 super-task kernel.
+//
+// Built from the cell list on cells of edge >= rc + skin, so every pair that
+// can come within rc before the next rebuild (no particle moved more than
+// skin/2) lies in the home cell's 14-entry half shell and is within rc + skin
+// now.  The list of a home cell is stored as a ROUND TABLE instead of per-
+// particle rows:
+//
+//   imap[cell][lane]          home particle served by this lane (lanes of one
+//                             particle contiguous; 0xFF = idle lane)
+//   desc[cell][round][lane]   partner j as (stencil entry << 8 | index in the
+//                             source cell), VL_IDLE = no pair this round
+//   nround[cell]
+//
+// with at most one pair per lane per round and no j twice in a round.  The
+// force kernel (verlet_rounds in cs_force2.cuh) then keeps F_i in registers
+// and writes the Newton-3 reaction on j without conflicts.  Lanes are shared
+// out in proportion to the particles' list lengths; pairs are dealt round-
+// robin to a particle's lanes, then placed first-fit into rounds by all lanes
+// in lockstep (a (j, round) collision is won by the lowest lane, so the
+// table -- and the force summation order -- is deterministic).
+//
+// Between rebuilds positions are not wrapped (the image shift of a stencil
+// entry is fixed at build time); cs_vv_kick_drift_track raises a flag once
+// any particle has moved more than skin/2 from its position at the build.
+#pragma once
+#include "cs_force2.cuh"
+
+#define VB_NW 4      // warps per builder CTA
+#define VB_JCAP 448  // candidate j per home cell (14 source cells)
+
+struct VList {
+  int32_t *nround;  // rounds R of the cell's table
+  uint8_t *imap;    // [cell][96]: lane -> first particle, second particle, switch round
+  uint16_t *desc;   // [cell][VL_RMAX][32]
+};
+
+static size_t vl_bytes(int64_t ncell) {
+  return cs_ws_slice(sizeof(int32_t) * ncell) + cs_ws_slice(96 * (size_t)ncell) +
+         cs_ws_slice(sizeof(uint16_t) * (size_t)VL_RMAX * 32 * ncell);
+}
+
+static VList vl_view(void *p, int64_t ncell) {
+  char *c = (char *)p;
+  VList v;
+  v.nround = (int32_t *)c;
+  c += cs_ws_slice(sizeof(int32_t) * ncell);
+  v.imap = (uint8_t *)c;
+  c += cs_ws_slice(96 * (size_t)ncell);
+  v.desc = (uint16_t *)c;
+  return v;
+}
+
+static void vl_attach(ForceArgs &A, const void *vlist) {
+  VList v = vl_view(const_cast<void *>(vlist), A.b.ncells);
+  A.vl_nround = v.nround;
+  A.vl_imap = v.imap;
+  A.vl_desc = v.desc;
+}
+
+extern "C" size_t cs_verlet_list_bytes(const cs_box *bx) {
+  Box b;
+  if (make_box(bx, &b) != CS_OK) return 0;
+  return vl_bytes(b.ncells);
+}
+
+// source cell of stencil entry e for home cell (h0, h1, h2): start, count
+// (0 if outside a non-periodic box) and the periodic image shift
+__device__ __forceinline__ void vl_source(const Box &b, const int32_t *start, int h0, int h1,
+                                          int h2, int e, int *st, int *cnt, double &s0,
+                                          double &s1, double &s2) {
+  int v0 = h0 + c_stencil3.o[e][0], v1 = h1 + c_stencil3.o[e][1], v2 = h2 + c_stencil3.o[e][2];
+  s0 = s1 = s2 = 0.0;
+  bool ok = true;
+  if (b.per[0]) { s0 = v0 >= b.nc[0] ? b.L[0] : (v0 < 0 ? -b.L[0] : 0.0); v0 = wrap1i(v0, b.nc[0]); }
+  else ok = ok && v0 >= 0 && v0 < b.nc[0];
+  if (b.per[1]) { s1 = v1 >= b.nc[1] ? b.L[1] : (v1 < 0 ? -b.L[1] : 0.0); v1 = wrap1i(v1, b.nc[1]); }
+  else ok = ok && v1 >= 0 && v1 < b.nc[1];
+  if (b.per[2]) { s2 = v2 >= b.nc[2] ? b.L[2] : (v2 < 0 ? -b.L[2] : 0.0); v2 = wrap1i(v2, b.nc[2]); }
+  else ok = ok && v2 >= 0 && v2 < b.nc[2];
+  *st = 0;
+  *cnt = 0;
+  if (ok) {
+    const int64_t gc = box_cell(b, v0, v1, v2);
+    *st = start[gc];
+    *cnt = start[gc + 1] - *st;
+  }
+}
+
+#define VB_NCH (VB_JCAP / 32)  // candidate chunks per home cell
+#define VB_SEG 4                // table lanes a particle may span
+
+struct VBuildSmem {
+  uint16_t tab[VB_NW][VL_RMAX][32];         // round table of the current cell
+  unsigned long long used[VB_NW][VB_JCAP];  // per candidate j: rounds taken
+  unsigned row[VB_NW][32][VB_NCH];          // particle -> candidate bits per chunk
+  uint16_t code[VB_NW][VB_JCAP];            // entry << 8 | index in the source cell
+  double hx[VB_NW][32][3];                  // home positions (broadcast reads)
+  uint8_t lmap[VB_NW][96];                  // lane -> first / second particle, switch round
+};
+
+// Lockstep first-fit: lane p places all pairs of particle p (row bits over the
+// candidate chunks) into its own slots -- up to VB_SEG segments (table lane
+// seg_l[k], free rounds fr[k]) -- taking the first segment with a free round
+// that does not hold the same j yet, lowest round first.  Equal (j, round)
+// proposals are won by the lowest lane; lanes start at different j so that
+// such collisions are rare.  Returns false (warp-uniform) if a pair found no
+// slot.
+__device__ __forceinline__ int vl_ffs(unsigned v) { return __ffs(v); }
+__device__ __forceinline__ int vl_ffs(unsigned long long v) { return __ffsll((long long)v); }
+
+template <class M>  // round masks: 32 bits while R <= 32, else 64
+__device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
+                                         const int *seg_l, unsigned long long *used,
+                                         const uint16_t *code, uint16_t (*tab)[32], int lane) {
+  bool ok = true;
+  int cc = 0;
+  unsigned cur = nch > 0 ? row[0] : 0u;
+  const int rot = (lane * 7) & 31;
+  while (true) {
+    while (cur == 0 && cc + 1 < nch) cur = row[++cc];
+    if (!__any_sync(CS_FULL, cur != 0)) break;
+    const bool act = cur != 0;
+    const unsigned hi = cur & (~0u << rot);
+    const int b = act ? __ffs(hi ? hi : cur) - 1 : 0;
+    const int jl = cc * 32 + b;
+    int r = -1, k = 0;
+    if (act) {
+      const M u = (M)used[jl];
+#pragma unroll
+      for (int kk = VB_SEG - 1; kk >= 0; --kk) {  // first segment with a free round wins
+        const M m = fr[kk] & ~u;
+        if (m) {
+          r = vl_ffs(m) - 1;
+          k = kk;
+        }
+      }
+      if (r < 0) {
+        ok = false;
+        cur = 0;
+        cc = nch;
+      }
+    }
+    const unsigned key = r >= 0 ? (unsigned)((jl << 6) | r) : (0x80000000u | lane);
+    const unsigned peers = __match_any_sync(CS_FULL, key);
+    __syncwarp();
+    if (r >= 0 && __ffs(peers) - 1 == lane) {
+      int tl = seg_l[0];
+#pragma unroll
+      for (int kk = 0; kk < VB_SEG; ++kk)
+        if (kk == k) {
+          fr[kk] &= ~((M)1 << r);
+          tl = seg_l[kk];
+        }
+      cur &= ~(1u << b);
+      tab[r][tl] = code[jl];
+      atomicOr(&used[jl], 1ull << r);
+    }
+    __syncwarp();
+  }
+  return __all_sync(CS_FULL, ok);
+}
+
+__global__ void __launch_bounds__(VB_NW * 32) k_verlet_build(Box b, const int32_t *start,
+                                                             const double *x, const double *y,
+                                                             const double *z, double rl2,
+                                                             VList L, unsigned *status) {
+  __shared__ VBuildSmem S;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < VB_NW * VL_RMAX * 32; k += blockDim.x) (&S.tab[0][0][0])[k] = VL_IDLE;
+  __syncthreads();
+  const int64_t nhome = (int64_t)b.owned_x * b.nc[1] * b.nc[2];
+  for (int64_t t = (int64_t)blockIdx.x * VB_NW + w; t < nhome; t += (int64_t)gridDim.x * VB_NW) {
+    const int h0 = (int)(t % b.owned_x), h1 = (int)((t / b.owned_x) % b.nc[1]),
+              h2 = (int)(t / ((int64_t)b.owned_x * b.nc[1]));
+    const int64_t cell = box_cell(b, h0, h1, h2);
+    int st = 0, cnt = 0;
+    double s0 = 0, s1 = 0, s2 = 0;
+    if (lane < 14) vl_source(b, start, h0, h1, h2, lane, &st, &cnt, s0, s1, s2);
+    const int na = __shfl_sync(CS_FULL, cnt, 0), a0 = __shfl_sync(CS_FULL, st, 0);
+    int incl = cnt;
+#pragma unroll
+    for (int k = 1; k < 16; k <<= 1) {
+      const int v = __shfl_up_sync(CS_FULL, incl, k);
+      if (lane >= k) incl += v;
+    }
+    const int excl = incl - cnt;
+    const int nj = __shfl_sync(CS_FULL, incl, 13);
+    const int nch = (nj + 31) / 32;
+    uint8_t *lm = L.imap + cell * 96;
+    if (na == 0 || na > 32 || nj > VB_JCAP) {
+      if (na > 32 || nj > VB_JCAP) atomicOr(status, 2u);
+      if (lane == 0) L.nround[cell] = 0;
+      lm[lane] = lm[32 + lane] = 0xFF;
+      continue;
+    }
+    if (lane < na) {
+      S.hx[w][lane][0] = __ldg(x + a0 + lane);
+      S.hx[w][lane][1] = __ldg(y + a0 + lane);
+      S.hx[w][lane][2] = __ldg(z + a0 + lane);
+    }
+    __syncwarp();
+    // pass 1: candidates (lane = j) -> rows (lane = home particle), list lengths
+    int len = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int tj = c * 32 + lane;
+      int e = 0;
+#pragma unroll
+      for (int k = 8; k >= 1; k >>= 1) {
+        const int cand = e + k;
+        const int ex = __shfl_sync(CS_FULL, excl, cand < 14 ? cand : 13);
+        if (cand < 14 && ex <= tj) e = cand;
+      }
+      const int q = tj - __shfl_sync(CS_FULL, excl, e);
+      const int sst = __shfl_sync(CS_FULL, st, e);
+      const double sx = __shfl_sync(CS_FULL, s0, e), sy = __shfl_sync(CS_FULL, s1, e),
+                   sz = __shfl_sync(CS_FULL, s2, e);
+      unsigned mask = 0;
+      if (tj < nj) {
+        const double xj = __ldg(x + sst + q) + sx, yj = __ldg(y + sst + q) + sy,
+                     zj = __ldg(z + sst + q) + sz;
+        const int ilim = e == 0 ? q : na;  // intra: pairs i < j only
+        for (int i = 0; i < ilim; ++i) {
+          const double dx = S.hx[w][i][0] - xj, dy = S.hx[w][i][1] - yj, dz = S.hx[w][i][2] - zj;
+          const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+          mask |= (unsigned)(r2 < rl2) << i;
+        }
+        S.code[w][tj] = (uint16_t)((e << 8) | q);
+      }
+      for (int i = 0; i < na; ++i) {
+        const unsigned bal = __ballot_sync(CS_FULL, (mask >> i) & 1u);
+        if (lane == i) {
+          S.row[w][i][c] = bal;
+          len += __popc(bal);
+        }
+      }
+    }
+    const int n = lane < na ? len + 1 + len / 16 : 0;  // slots: pairs + slack
+    const int P = warp_sum(n);
+    if (warp_sum(len) == 0) {
+      if (lane == 0) L.nround[cell] = 0;
+      lm[lane] = lm[32 + lane] = 0xFF;
+      continue;
+    }
+    // at most VB_SEG table lanes per particle: n <= (VB_SEG - 1) R + 1
+    int R = max((P + 31) / 32, ((int)__reduce_max_sync(CS_FULL, (unsigned)n) + VB_SEG - 3) / (VB_SEG - 1));
+    bool placed = false;
+    while (!placed && R <= VL_RMAX) {
+      // lane-major layout: particles in order, at most two per table lane (a
+      // particle that would be the third in a lane starts the next one)
+      int Lc = 0, off = 0, segs = 0, cL = 0, cO = 0;
+      for (int p = 0; p < na; ++p) {
+        int rest = __shfl_sync(CS_FULL, n, p);
+        if (off != 0 && segs >= 2) {
+          ++Lc;
+          off = segs = 0;
+        }
+        if (lane == p) {
+          cL = Lc;
+          cO = off;
+        }
+        const int take = min(rest, R - off);
+        rest -= take;
+        off += take;
+        ++segs;
+        if (off == R) {
+          ++Lc;
+          off = segs = 0;
+        }
+        if (rest > 0) {
+          Lc += rest / R;
+          off = rest % R;
+          segs = off ? 1 : 0;
+        }
+      }
+      if (Lc + (off ? 1 : 0) > 32) {
+        ++R;
+        continue;
+      }
+      // this particle's segments: table lanes cL, cL + 1, ... with free rounds
+      unsigned long long fr[VB_SEG];
+      int seg_l[VB_SEG];
+      {
+        int rest = n, lo = cO;
+#pragma unroll
+        for (int k = 0; k < VB_SEG; ++k) {
+          const int hi = min(R, lo + rest);
+          const int w2 = hi - lo;
+          fr[k] = w2 > 0 ? (((w2 >= 64 ? ~0ull : ((1ull << w2) - 1))) << lo) : 0ull;
+          seg_l[k] = min(cL + k, 31);
+          rest -= max(w2, 0);
+          lo = 0;
+        }
+      }
+      // lane -> (first particle, second particle, switch round)
+      S.lmap[w][lane] = S.lmap[w][32 + lane] = 0xFF;
+      S.lmap[w][64 + lane] = (uint8_t)R;
+      for (int j = lane; j < nj; j += 32) S.used[w][j] = 0ull;
+      __syncwarp();
+      if (lane < na) {
+        if (cO != 0) {
+          S.lmap[w][32 + cL] = (uint8_t)lane;
+          S.lmap[w][64 + cL] = (uint8_t)cO;
+        } else {
+          S.lmap[w][cL] = (uint8_t)lane;
+        }
+#pragma unroll
+        for (int k = 1; k < VB_SEG; ++k)
+          if (fr[k]) S.lmap[w][seg_l[k]] = (uint8_t)lane;
+      }
+      __syncwarp();
+      // pass 2: place the pairs
+      bool ok;
+      if (R <= 32) {
+        unsigned f32[VB_SEG];
+#pragma unroll
+        for (int k = 0; k < VB_SEG; ++k) f32[k] = (unsigned)fr[k];
+        ok = vl_place(S.row[w][lane < na ? lane : 0], lane < na ? nch : 0, f32, seg_l, S.used[w],
+                      S.code[w], S.tab[w], lane);
+      } else {
+        ok = vl_place(S.row[w][lane < na ? lane : 0], lane < na ? nch : 0, fr, seg_l, S.used[w],
+                      S.code[w], S.tab[w], lane);
+      }
+      if (ok) {
+        placed = true;
+      } else {  // a pair found no free round: clear and retry with one more round
+        for (int r = 0; r < R; ++r) S.tab[w][r][lane] = VL_IDLE;
+        __syncwarp();
+        ++R;
+      }
+    }
+    if (!placed) {
+      if (lane == 0) {
+        atomicOr(status, 4u);
+        L.nround[cell] = 0;
+      }
+      lm[lane] = lm[32 + lane] = 0xFF;
+      continue;
+    }
+    if (lane == 0) L.nround[cell] = R;
+    lm[lane] = S.lmap[w][lane];
+    lm[32 + lane] = S.lmap[w][32 + lane];
+    lm[64 + lane] = S.lmap[w][64 + lane];
+    uint16_t *dst = L.desc + cell * (VL_RMAX * 32) + lane;
+    for (int r = 0; r < R; ++r) {
+      dst[r * 32] = S.tab[w][r][lane];
+      S.tab[w][r][lane] = VL_IDLE;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_wrap_copy(int64_t n, double Lx, double Ly, double Lz, double *x, double *y,
+                            double *z) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = wrap_dev(x[i], Lx);
+    y[i] = wrap_dev(y[i], Ly);
+    z[i] = wrap_dev(z[i], Lz);
+  }
+}
+
+__global__ void k_copy3(int64_t n, const double *x, const double *y, const double *z, double *xo,
+                        double *yo, double *zo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    xo[i] = x[i];
+    yo[i] = y[i];
+    zo[i] = z[i];
+  }
+}
+
+// kick + drift without wrapping; flag = 1 once a particle is more than
+// sqrt(lim2) from its position at the last list build
+__global__ void k_kick_drift_track(int64_t n, double hdtm, double dt, const double *fx,
+                                   const double *fy, const double *fz, double *vx, double *vy,
+                                   double *vz, double *x, double *y, double *z, const double *x0,
+                                   const double *y0, const double *z0, double lim2, int32_t *flag) {
+  bool far = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double ux = __fma_rn(hdtm, fx[i], vx[i]);
+    const double uy = __fma_rn(hdtm, fy[i], vy[i]);
+    const double uz = __fma_rn(hdtm, fz[i], vz[i]);
+    vx[i] = ux;
+    vy[i] = uy;
+    vz[i] = uz;
+    const double nx = __fma_rn(dt, ux, x[i]), ny = __fma_rn(dt, uy, y[i]), nz = __fma_rn(dt, uz, z[i]);
+    x[i] = nx;
+    y[i] = ny;
+    z[i] = nz;
+    const double dx = nx - x0[i], dy = ny - y0[i], dz = nz - z0[i];
+    far |= __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx)) > lim2;
+  }
+  if (__any_sync(CS_FULL, far) && (threadIdx.x & 31) == 0) *flag = 1;  // same value from every writer
+}
+
+extern "C" int cs_wrap_positions(int64_t n, const cs_box *b, double *x, double *y, double *z,
+                                 void *stream) {
+  if (n <= 0) return CS_OK;
+  k_wrap_copy<<<grid_for(n, 256), 256, 0, cs_stream(stream)>>>(n, b->L[0], b->L[1], b->L[2], x, y, z);
+  return cs_check_launch("wrap_positions");
+}
+
+extern "C" int cs_vv_kick_drift_track(int64_t n, double hdtm, double dt, const double *fx,
+                                      const double *fy, const double *fz, double *vx, double *vy,
+                                      double *vz, double *x, double *y, double *z,
+                                      const double *x0, const double *y0, const double *z0,
+                                      double half_skin, int32_t *flag, void *stream) {
+  if (n <= 0) return CS_OK;
+  k_kick_drift_track<<<grid_for(n, 256), 256, 0, cs_stream(stream)>>>(
+      n, hdtm, dt, fx, fy, fz, vx, vy, vz, x, y, z, x0, y0, z0, half_skin * half_skin, flag);
+  return cs_check_launch("vv_kick_drift_track");
+}
+
+extern "C" int cs_verlet_build(const cs_box *bx, const cs_lj *lj, double skin,
+                               const int32_t *cell_start, const double *x, const double *y,
+                               const double *z, void *list, size_t list_bytes, double *x0,
+                               double *y0, double *z0, int64_t n, unsigned *status_dev,
+                               void *stream) {
+  CS_TRY(cs_upload_stencil());
+  cudaStream_t st = cs_stream(stream);
+  Box b;
+  CS_TRY(make_box(bx, &b));
+  CS_REQUIRE(skin >= 0, "skin must be >= 0");
+  for (int k = 0; k < 3; ++k) {
+    CS_REQUIRE(b.gnc[k] >= 3, "Verlet lists need >= 3 cells per axis");
+    CS_REQUIRE(b.L[k] / b.gnc[k] >= (lj->rc + skin) * (1 - 1e-12),
+               "cell edge %.6g on axis %d is below rc + skin = %.6g", b.L[k] / b.gnc[k], k,
+               lj->rc + skin);
+  }
+  CS_REQUIRE(list_bytes >= vl_bytes(b.ncells), "Verlet list buffer too small (%zu < %zu)",
+             list_bytes, vl_bytes(b.ncells));
+  CS_REQUIRE(status_dev, "status pointer required");
+  VList L = vl_view(list, b.ncells);
+  const double rl = lj->rc + skin;
+  const double rl2 = rl * rl * (1.0 + 1e-12);
+  const int64_t nhome = (int64_t)b.owned_x * b.nc[1] * b.nc[2];
+  const int64_t blocks = (nhome + VB_NW - 1) / VB_NW;
+  if (b.ncells > nhome) {  // ghost cells own no home tasks
+    CS_CUDA(cudaMemsetAsync(L.nround, 0, sizeof(int32_t) * b.ncells, st));
+  }
+  if (blocks > 0)
+    k_verlet_build<<<(unsigned)blocks, VB_NW * 32, 0, st>>>(b, cell_start, x, y, z, rl2, L, status_dev);
+  if (x0 && n > 0) k_copy3<<<grid_for(n, 256), 256, 0, st>>>(n, x, y, z, x0, y0, z0);
+  return cs_check_launch("verlet_build");
+}
+
+extern "C" int cs_lj_forces_verlet(const cs_box *bx, const cs_lj *lj, int sched, int64_t npart,
+                                   const int32_t *cell_start, const void *list, const double *x,
+                                   const double *y, const double *z, double *fx, double *fy,
+                                   double *fz, double *energy_dev, unsigned long long *npairs_dev,
+                                   unsigned *status_dev, void *ws, size_t ws_bytes, void *stream) {
+  CS_REQUIRE(list, "null Verlet list");
+  return lj_forces_impl(bx, lj, sched, npart, cell_start, list, x, y, z, fx, fy, fz, energy_dev,
+                        npairs_dev, status_dev, ws, ws_bytes, cs_stream(stream));
+}
+
+// ------------------------------------------------ in-place rebinning helper --
+__global__ void k_copy7(int64_t n, const double *x, const double *y, const double *z,
+                        const double *vx, const double *vy, const double *vz, const int32_t *id,
+                        double *xo, double *yo, double *zo, double *vxo, double *vyo,
+                        double *vzo, int32_t *ido) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    xo[i] = x[i];
+    yo[i] = y[i];
+    zo[i] = z[i];
+    vxo[i] = vx[i];
+    vyo[i] = vy[i];
+    vzo[i] = vz[i];
+    ido[i] = id[i];
+  }
+}
+
+extern "C" int cs_copy7(int64_t n, const double *x, const double *y, const double *z,
+                        const double *vx, const double *vy, const double *vz, const int32_t *id,
+                        double *xo, double *yo, double *zo, double *vxo, double *vyo, double *vzo,
+                        int32_t *ido, void *stream) {
+  if (n <= 0) return CS_OK;
+  k_copy7<<<grid_for(n, 256), 256, 0, cs_stream(stream)>>>(n, x, y, z, vx, vy, vz, id, xo, yo,
+                                                            zo, vxo, vyo, vzo, ido);
+  return cs_check_launch("copy7");
+}
+
+// ------------------------------- conditional rebuild inside a CUDA graph --
+// The rebuild decision stays on the device: a one-thread kernel turns the
+// displacement flag into the graph's IF condition (and clears the flag), and
+// the rebuild work is captured into the body of that conditional node.
+__global__ void k_set_cond(cudaGraphConditionalHandle h, int32_t *flag, int32_t *count) {
+  const int32_t v = *flag;
+  *flag = 0;
+  if (v && count) ++*count;
+  cudaGraphSetConditional(h, v ? 1u : 0u);
+}
+
+extern "C" int cs_capture_if_begin(void *stream, void *side_stream, int32_t *flag,
+                                   int32_t *count) {
+  cudaStream_t st = cs_stream(stream), side = cs_stream(side_stream);
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t *deps = nullptr;
+  size_t nd = 0;
+  CS_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  CS_REQUIRE(cs == cudaStreamCaptureStatusActive, "cs_capture_if_begin: stream is not capturing");
+  cudaGraphConditionalHandle h;
+  CS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  k_set_cond<<<1, 1, 0, st>>>(h, flag, count);
+  CS_TRY(cs_check_launch("set_cond"));
+  CS_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  alignas(cudaGraphNodeParams) unsigned char pbuf[sizeof(cudaGraphNodeParams)];
+  memset(pbuf, 0, sizeof(pbuf));  // (the union has no default constructor)
+  cudaGraphNodeParams &p = *reinterpret_cast<cudaGraphNodeParams *>(pbuf);
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeIf;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  CS_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  CS_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  CS_CUDA(cudaStreamBeginCaptureToGraph(side, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  return CS_OK;
+}
+
+extern "C" int cs_capture_if_end(void *side_stream) {
+  cudaGraph_t g;
+  CS_CUDA(cudaStreamEndCapture(cs_stream(side_stream), &g));
+  return CS_OK;
+}

@@ -24,7 +24,11 @@ from . import _lib
 from .grid import GridSpec
 
 SCHEDULES = {"loopex": _lib.SCHED_LOOPEX, "block": _lib.SCHED_BLOCK, "shell": _lib.SCHED_SHELL,
-             "buffered": _lib.SCHED_BUFFERED}
+             "buffered": _lib.SCHED_BUFFERED,
+             # Verlet lists on cells of edge >= rc + skin, under the
+             # buffered or the in-place colour-pass block structure
+             "verlet": _lib.SCHED_BUFFERED, "verlet_shell": _lib.SCHED_SHELL}
+VERLET_SCHEDULES = ("verlet", "verlet_shell")
 
 
 def _torch():
@@ -114,18 +118,23 @@ class LJSystem:
     """Particles + cell list + workspaces on one GPU (single periodic domain)."""
 
     def __init__(self, box: LJBox, n: int, params: LJParams = LJParams(), schedule: str = "block",
-                 block=None, device=None):
+                 block=None, device=None, skin: float = 0.3):
         torch = _torch()
         _lib.require_cuda()
         if schedule not in SCHEDULES:
             raise ValueError(f"schedule must be one of {tuple(SCHEDULES)}")
+        self.verlet = schedule in VERLET_SCHEDULES
+        self.skin = float(skin) if self.verlet else 0.0
+        if self.skin < 0:
+            raise ValueError("skin must be >= 0")
         for e in box.cell_edge:
-            if e < params.rc * (1 - 1e-12):
-                raise ValueError(f"cell edge {e} below cutoff {params.rc}")
+            if e < (params.rc + self.skin) * (1 - 1e-12):
+                raise ValueError(f"cell edge {e} below cutoff {params.rc}"
+                                 + (f" + skin {self.skin}" if self.verlet else ""))
         self.box, self.params, self.n = box, params, int(n)
         self.schedule = schedule
         even = all(c % 2 == 0 for c in box.cells)
-        if schedule in ("shell", "buffered"):
+        if schedule in ("shell", "buffered") or self.verlet:
             self.block = tuple(block) if block is not None else (2, 2, 2)
         elif schedule == "block":
             self.block = tuple(block) if block is not None else choose_block(box.cells)
@@ -158,6 +167,14 @@ class LJSystem:
         self.status = torch.zeros(1, dtype=torch.int32, device=d)  # kernel capacity flags
         self.dt = 0.005
         self._graphs = {}
+        self._capturing = False
+        if self.verlet:
+            nb = int(L.cs_verlet_list_bytes(C.byref(self._cbox)))
+            self.vlist = torch.zeros(nb, dtype=torch.uint8, device=d)
+            self.xref = [torch.zeros(max(self.n, 1), dtype=f64, device=d) for _ in range(3)]
+            self.vflag = torch.zeros(1, dtype=i32, device=d)  # displacement > skin/2
+            self.graph_builds = torch.zeros(1, dtype=i32, device=d)  # rebuilds taken inside graphs
+            self.list_builds = 0  # host-side count (eager steps and explicit rebuilds)
 
     # ----------------------------------------------------------- plumbing
     def _make_cbox(self):
@@ -194,12 +211,14 @@ class LJSystem:
     @classmethod
     def fcc(cls, n_unit_cells=6, density: float = 0.8442, temperature: float = 0.722,
             jitter: float = 0.05, seed: int = 42, params: LJParams = LJParams(),
-            schedule: str = "block", block=None, dt: float = 0.005):
+            schedule: str = "block", block=None, dt: float = 0.005, skin: float = 0.3):
         """FCC lattice + seeded uniform jitter + Gaussian velocities at T
-        (momentum removed, 3N-3 dof), then cell list + initial forces."""
-        box, nuc, a = fcc_box(n_unit_cells, density, params.rc)
+        (momentum removed, 3N-3 dof), then cell list + initial forces.
+        Verlet schedules bin on cells of edge >= rc + skin."""
+        verlet = schedule in VERLET_SCHEDULES
+        box, nuc, a = fcc_box(n_unit_cells, density, params.rc + (skin if verlet else 0.0))
         n = 4 * nuc[0] * nuc[1] * nuc[2]
-        s = cls(box, n, params, schedule, block)
+        s = cls(box, n, params, schedule, block, skin=skin)
         s.dt = dt
         s.seed_fcc(nuc, a, temperature, jitter, seed)
         return s
@@ -228,8 +247,26 @@ class LJSystem:
         self.rebuild()
 
     def rebuild(self, energy: bool = True):
-        self.build_cells()
+        if self.verlet:
+            self._rebuild_list()
+        else:
+            self.build_cells()
         self.compute_forces(energy=energy)
+
+    def _rebuild_list(self):
+        """Verlet mode: wrap, rebin in place, rebuild the round tables and
+        remember the positions for the displacement check."""
+        b = self._buf[self.cur]
+        _lib.call("cs_wrap_positions", self.n, C.byref(self._cbox), _lib.ptr(b["x"]), _lib.ptr(b["y"]),
+                  _lib.ptr(b["z"]), self._s())
+        self.build_cells()
+        b = self._buf[self.cur]
+        _lib.call("cs_verlet_build", C.byref(self._cbox), C.byref(self._clj), self.skin,
+                  _lib.ptr(self.cell_start), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]),
+                  _lib.ptr(self.vlist), self.vlist.numel(), *(_lib.ptr(t) for t in self.xref),
+                  self.n, _lib.ptr(self.status), self._s())
+        if not self._capturing:
+            self.list_builds += 1
 
     # ------------------------------------------------------------- kernels
     def build_cells(self):
@@ -241,7 +278,12 @@ class LJSystem:
                   _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]), _lib.ptr(b["id"]),
                   _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), _lib.ptr(self.cell_start),
                   _lib.ptr(self._ws), self._wsb, self._s())
-        self.cur = 1 - self.cur
+        if self.verlet:  # in place: the rebuild may sit inside a conditional graph node
+            ks = ("x", "y", "z", "vx", "vy", "vz", "id")
+            _lib.call("cs_copy7", self.n, *(_lib.ptr(b[k]) for k in ks), *(_lib.ptr(a[k]) for k in ks),
+                      self._s())
+        else:
+            self.cur = 1 - self.cur
 
     def compute_forces(self, energy: bool = False, count_pairs: bool = True):
         """K2 (forces must be zero on entry; build_cells zeroes them)."""
@@ -250,6 +292,14 @@ class LJSystem:
             self.scal[0:1].zero_()
         if count_pairs:
             self.npairs.zero_()
+        if self.verlet:
+            _lib.call("cs_lj_forces_verlet", C.byref(self._cbox), C.byref(self._clj),
+                      SCHEDULES[self.schedule], self.n, _lib.ptr(self.cell_start), _lib.ptr(self.vlist),
+                      _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]), _lib.ptr(b["fx"]),
+                      _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), _lib.ptr(self.scal) if energy else None,
+                      _lib.ptr(self.npairs) if count_pairs else None, _lib.ptr(self.status),
+                      _lib.ptr(self._ws), self._wsb, self._s())
+            return
         _lib.call("cs_lj_forces", C.byref(self._cbox), C.byref(self._clj), SCHEDULES[self.schedule],
                   self.n, _lib.ptr(self.cell_start), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]),
                   _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]),
@@ -262,9 +312,40 @@ class LJSystem:
         _lib.call("cs_kinetic", self.n, self.params.mass, _lib.ptr(b["vx"]), _lib.ptr(b["vy"]),
                   _lib.ptr(b["vz"]), _lib.ptr(self.scal[1:]), _lib.ptr(self._ws), self._wsb, self._s())
 
+    def _pre_verlet(self):
+        """Verlet mode: kick + drift (no wrap) with the displacement check, then
+        the list rebuild if any particle moved more than skin/2 -- decided on
+        the host when eager, by a conditional graph node when captured."""
+        torch = _torch()
+        hdtm = 0.5 * self.dt / self.params.mass
+        b = self._buf[self.cur]
+        _lib.call("cs_vv_kick_drift_track", self.n, hdtm, self.dt, _lib.ptr(b["fx"]), _lib.ptr(b["fy"]),
+                  _lib.ptr(b["fz"]), _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]),
+                  _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]), *(_lib.ptr(t) for t in self.xref),
+                  0.5 * self.skin, _lib.ptr(self.vflag), self._s())
+        if self._capturing:
+            side = self._side
+            _lib.call("cs_capture_if_begin", self._s(), side.cuda_stream, _lib.ptr(self.vflag),
+                      _lib.ptr(self.graph_builds))
+            with torch.cuda.stream(side):
+                self._rebuild_list()
+            _lib.call("cs_capture_if_end", side.cuda_stream)
+        elif int(self.vflag.item()):
+            self.vflag.zero_()
+            self._rebuild_list()
+
     def step(self, energy: bool = False):
         """One velocity-Verlet step (K3 kick+drift, K1, K2, K3 kick)."""
         hdtm = 0.5 * self.dt / self.params.mass
+        if self.verlet:
+            self._pre_verlet()
+            self.compute_forces(energy=energy)
+            b = self._buf[self.cur]
+            _lib.call("cs_vv_kick", self.n, hdtm, _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]),
+                      _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]), self._s())
+            if energy:
+                self.kinetic()
+            return
         b = self._buf[self.cur]
         _lib.call("cs_vv_kick_drift", self.n, hdtm, self.dt, C.byref(self._cbox), _lib.ptr(b["fx"]),
                   _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), _lib.ptr(b["vx"]), _lib.ptr(b["vy"]),
@@ -288,10 +369,15 @@ class LJSystem:
             start = self.cur
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream(device=self.device)
+            self._side = torch.cuda.Stream(device=self.device)
             s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                with torch.cuda.graph(g, stream=s):
-                    fn()
+            self._capturing = True
+            try:
+                with torch.cuda.stream(s):
+                    with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+                        fn()
+            finally:
+                self._capturing = False
             torch.cuda.current_stream().wait_stream(s)
             self._graphs[gkey] = (g, self.cur)
             self.cur = start
@@ -309,6 +395,9 @@ class LJSystem:
         hdtm = 0.5 * self.dt / self.params.mass
 
         def pre():
+            if self.verlet:
+                self._pre_verlet()
+                return
             b = self._buf[self.cur]
             _lib.call("cs_vv_kick_drift", self.n, hdtm, self.dt, C.byref(self._cbox),
                       _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), _lib.ptr(b["vx"]),
@@ -329,6 +418,9 @@ class LJSystem:
     def launches_per_step(self, energy: bool = False) -> int:
         """Kernels this package launches per step (memsets excluded)."""
         build = 1 + 3 + 1 + 1  # count, scan x3, scatter, sort-gather
+        if self.verlet:  # kick_drift_track, set_cond, buffered force (sizes, scan x3, force, gather), reduce x2, kick
+            force = (1 + 3 + 1 + 1) if self.schedule == "verlet" else 8
+            return 2 + force + 2 + 1 + (3 if energy else 0)
         force = (27 if self.schedule == "loopex" else 8) + 2  # passes + pair/energy reduce
         return 1 + build + force + 1 + (3 if energy else 0)
 
@@ -346,6 +438,26 @@ class LJSystem:
             nb = np.roll(cnt, shift=(-oz, -oy, -ox), axis=(0, 1, 2))
             c += int((cnt * nb).sum())
         return c
+
+    def list_pairs(self) -> int:
+        """Verlet mode: pairs held in the current round tables (each is
+        distance-tested every step; the C of the 8 C + 20 P convention)."""
+        torch = _torch()
+        nc = self.box.cell_count
+        sl = lambda b: (b + 255) // 256 * 256  # cs_ws_slice, layout of vl_view
+        o2 = sl(4 * nc) + sl(96 * nc)
+        nr = self.vlist[: 4 * nc].view(torch.int32).long()
+        desc = self.vlist[o2: o2 + 2 * 64 * 32 * nc].view(torch.int16).view(nc, 64, 32)
+        live = torch.arange(64, device=self.device)[None, :] < nr[:, None]
+        return int(((desc != 0x0F00) & live[:, :, None]).sum())  # VL_IDLE
+
+    def list_rounds(self):
+        """Verlet mode: (rounds per cell as a host array, lane use)."""
+        torch = _torch()
+        nc = self.box.cell_count
+        nr = self.vlist[: 4 * nc].view(torch.int32).cpu().numpy()
+        rounds = nr
+        return rounds, self.list_pairs() / (32.0 * max(int(rounds.sum()), 1))
 
     def _state_tensors(self):
         out = []
@@ -367,10 +479,17 @@ class LJSystem:
     # -------------------------------------------------------------- output
     def check_status(self):
         """Raise if a kernel reported a capacity overflow (buffered schedule)."""
-        if int(self.status.item()):
+        st = int(self.status.item())
+        if st & 1:
             raise _lib.CellschedError(
                 "buffered force schedule: a block exceeded its shared-memory capacity; "
                 "use schedule='shell' (in-place fallback) for this density")
+        if st & 2:
+            raise _lib.CellschedError("Verlet list: a cell holds more than 32 particles; "
+                                      "use a link-cell schedule for this density")
+        if st & 4:
+            raise _lib.CellschedError("Verlet list: a home cell needs more than 64 rounds; "
+                                      "reduce the skin")
 
     def energies(self):
         """(PE, KE) of the last energy evaluation (synchronises)."""

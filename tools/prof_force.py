@@ -13,3 +13,8 @@ for _ in range(3):
     s.compute_forces(energy=False)
 torch.cuda.synchronize()
 print("pairs", s.pair_count())
+if s.verlet:
+    rounds, use = s.list_rounds()
+    lp = s.list_pairs()
+    print("rounds mean %.2f max %d  list pairs %d  lane use %.3f  hits/list %.3f"
+          % (rounds.mean(), rounds.max(), lp, use, s.pair_count() / lp))
