@@ -410,7 +410,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--schedule", default="buffered",
-                    choices=["shell", "buffered", "block", "loopex", "verlet", "verlet_shell"])
+                    choices=["shell", "buffered", "dataflow", "block", "loopex", "verlet", "verlet_shell",
+                             "verlet_dataflow"])
     ap.add_argument("--skin", type=float, default=0.3, help="Verlet skin (verlet schedules)")
     ap.add_argument("--block", type=lambda s: tuple(int(v) for v in s.split(",")), default=None)
     ap.add_argument("--no-cpu", action="store_true")

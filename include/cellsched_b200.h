@@ -149,7 +149,8 @@ int cs_payload_colour(const cs_grid *g, int sched, const int32_t *block_host, co
 size_t cs_payload_colour_ws_bytes(const cs_grid *g);
 
 /* ===================== LJ link-cell MD (new; extends the payload plug-in) */
-enum { CS_SCHED_LOOPEX = 0, CS_SCHED_BLOCK = 1, CS_SCHED_SHELL = 2, CS_SCHED_BUFFERED = 3 };
+enum { CS_SCHED_LOOPEX = 0, CS_SCHED_BLOCK = 1, CS_SCHED_SHELL = 2, CS_SCHED_BUFFERED = 3,
+       CS_SCHED_DATAFLOW = 4 };
 
 /* Local cell box.  Single GPU: nc == gnc, x0 == 0, periodic {1,1,1}.
  * x-slab rank: nc[0] = owned planes + 1 ghost plane, periodic[0] = 0,
@@ -200,7 +201,12 @@ int cs_build_cells(int64_t n, const cs_box *b, const double *x, const double *y,
  *                     home-cell half shell, per-offset reaction slots
  *   CS_SCHED_BUFFERED one pass over all blocks into private footprint
  *                     buffers + a deterministic gather (buffered strategy,
- *                     taskgen.py:237-276, at block granularity) */
+ *                     taskgen.py:237-276, at block granularity)
+ *   CS_SCHED_DATAFLOW the SHELL colour order executed as a dataflow: one
+ *                     persistent launch, blocks taken in (colour, block)
+ *                     order, each waiting only for its lower-colour
+ *                     neighbour blocks (the task dependencies of
+ *                     depgraph.py:28-49 at block granularity) */
 size_t cs_force_ws_bytes(const cs_box *b, int sched, int64_t n);
 int cs_lj_forces(const cs_box *b, const cs_lj *p, int sched, int64_t n,
                  const int32_t *cell_start, const double *x, const double *y, const double *z,

@@ -21,7 +21,7 @@ CS_ERANGE = -4
 CS_ECYCLE = -5
 
 STREAM_BASIC, STREAM_LOOPEX = 0, 1
-SCHED_LOOPEX, SCHED_BLOCK, SCHED_SHELL, SCHED_BUFFERED = 0, 1, 2, 3
+SCHED_LOOPEX, SCHED_BLOCK, SCHED_SHELL, SCHED_BUFFERED, SCHED_DATAFLOW = 0, 1, 2, 3, 4
 
 
 class CsGrid(C.Structure):

@@ -348,10 +348,10 @@ extern "C" size_t cs_force_ws_bytes(const cs_box *bx, int sched, int64_t n) {
   size_t base = cs_ws_slice(sizeof(double) * nc) + cs_ws_slice(sizeof(unsigned) * nc) +
                 cs_ws_slice(sizeof(double) * RED_BLOCKS_MAX) +
                 cs_ws_slice(sizeof(unsigned long long) * RED_BLOCKS_MAX);
-  if (sched == CS_SCHED_BUFFERED) {
+  if (sched == CS_SCHED_BUFFERED || sched == CS_SCHED_DATAFLOW) {
     Box b;
     if (make_box(bx, &b) != CS_OK) return 0;
-    base += shell_buffered_ws(b, n);
+    base += shell_buffered_ws(b, n);  // (covers the dataflow flags too)
   }
   return base;
 }
@@ -366,7 +366,12 @@ static int check_lj_box(const Box &b, double rc) {
   return CS_OK;
 }
 
-static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, bool verlet,
+// super-task kernel modes (cs_force2.cuh): 0 = colour pass (blockIdx = block
+// of that colour), 1 = buffered (blockIdx = block), 2 = dataflow (colour and
+// block from a ticket)
+enum { SH_COLOUR = 0, SH_BUFFERED = 1, SH_DATAFLOW = 2 };
+
+static int launch_shell_passes(const ForceArgs &A, bool energy, int mode, bool verlet,
                                cs_ws *w, int64_t n, unsigned *status, cudaStream_t st);
 
 // vlist: Verlet round tables (cs_verlet.cuh) or null for the link-cell path
@@ -420,16 +425,18 @@ static int lj_forces_impl(const cs_box *bx, const cs_lj *lj, int sched, int64_t 
   if (energy) CS_CUDA(cudaMemsetAsync(pe_cell, 0, sizeof(double) * nc, st));
   CS_CUDA(cudaMemsetAsync(hits_cell, 0, sizeof(unsigned) * nc, st));
   if (vlist) {
-    CS_REQUIRE(sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED,
-               "Verlet forces run under CS_SCHED_SHELL or CS_SCHED_BUFFERED");
+    CS_REQUIRE(sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED || sched == CS_SCHED_DATAFLOW,
+               "Verlet forces run under CS_SCHED_SHELL, CS_SCHED_BUFFERED or CS_SCHED_DATAFLOW");
     vl_attach(A, vlist);
     CS_TRY(block_grid(A.b, A.nbk));
-    if (sched == CS_SCHED_SHELL) {  // in-place colour passes accumulate: start from zero
+    if (sched != CS_SCHED_BUFFERED) {  // in-place passes accumulate: start from zero
       CS_CUDA(cudaMemsetAsync(fx, 0, sizeof(double) * npart, st));
       CS_CUDA(cudaMemsetAsync(fy, 0, sizeof(double) * npart, st));
       CS_CUDA(cudaMemsetAsync(fz, 0, sizeof(double) * npart, st));
     }
-    CS_TRY(launch_shell_passes(A, energy, sched == CS_SCHED_BUFFERED, true, &w, npart, status_dev, st));
+    CS_TRY(launch_shell_passes(A, energy, sched == CS_SCHED_BUFFERED ? SH_BUFFERED
+                                          : (sched == CS_SCHED_DATAFLOW ? SH_DATAFLOW : SH_COLOUR),
+                               true, &w, npart, status_dev, st));
   } else if (sched == CS_SCHED_LOOPEX) {
     for (int level = 0; level < 27; ++level) {
       int64_t ntask = (int64_t)A.b.owned_x * A.b.nc[1] * A.b.nc[2];  // upper bound
@@ -462,9 +469,11 @@ static int lj_forces_impl(const cs_box *bx, const cs_lj *lj, int sched, int64_t 
       else
         k_force_block<false><<<blocks, BLK_THREADS, smem, st>>>(A, colour);
     }
-  } else if (sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED) {
+  } else if (sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED || sched == CS_SCHED_DATAFLOW) {
     CS_TRY(block_grid(A.b, A.nbk));
-    CS_TRY(launch_shell_passes(A, energy, sched == CS_SCHED_BUFFERED, false, &w, npart, status_dev, st));
+    CS_TRY(launch_shell_passes(A, energy, sched == CS_SCHED_BUFFERED ? SH_BUFFERED
+                                          : (sched == CS_SCHED_DATAFLOW ? SH_DATAFLOW : SH_COLOUR),
+                               false, &w, npart, status_dev, st));
   } else {
     CS_REQUIRE(0, "unknown schedule %d", sched);
   }

@@ -240,6 +240,9 @@ struct ShellArgs {
   int64_t bufstride;
   unsigned *err;          // capacity overflow flag (buffered mode)
   int overwrite;          // buffered gather stores instead of adding (Verlet mode)
+  int *flags;             // dataflow mode: per block "published" flag
+  int *ticket;            // dataflow mode: next (colour, block) ticket
+  int coff[9];            // dataflow mode: first ticket of each colour
 };
 
 // block coordinates -> global cell of a footprint cell (or -1)
@@ -251,9 +254,11 @@ __device__ __forceinline__ int64_t foot_cell(const Box &b, const int *o0, int lc
   return box_cell(b, v0, v1, v2);
 }
 
-template <bool ENERGY, bool BUFFERED, bool VERLET>
-__global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int colour) {
-  extern __shared__ __align__(16) unsigned char sh_raw[];
+
+template <bool ENERGY, int MODE, bool VERLET>
+__device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *sh_raw, int colour,
+                                            int bid) {
+  constexpr bool BUFFERED = MODE == SH_BUFFERED;
   using SM = typename std::conditional<VERLET, ShellSmemVL, ShellSmem>::type;
   constexpr int RCAP = SM::RCAP, HCAP = SM::HCAP;
   SM &S = *reinterpret_cast<SM *>(sh_raw);
@@ -262,7 +267,6 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
   const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
   const int nhome = B0 * B1 * B2;
   int o0[3];
-  int bid = blockIdx.x;
   if (BUFFERED) {
     o0[0] = (bid % A.nbk[0]) * B0;
     o0[1] = ((bid / A.nbk[0]) % A.nbk[1]) * B1;
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
   }
   __syncthreads();
   if (S.overflow) {
-    if constexpr (BUFFERED) {  // no in-place fallback in buffered mode: report to the host
+    if constexpr (MODE != SH_COLOUR) {  // no in-place fallback: report to the host
       if (threadIdx.x == 0) atomicExch(SA.err, 1u);
       return;
     } else {
@@ -577,6 +581,10 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
         SA.buf[o] = sx;
         SA.buf[SA.bufstride + o] = sy;
         SA.buf[2 * SA.bufstride + o] = sz;
+      } else if (MODE == SH_DATAFLOW) {  // other SMs wrote f: read through L2
+        A.fx[g0 + i] = __ldcg(A.fx + g0 + i) + sx;
+        A.fy[g0 + i] = __ldcg(A.fy + g0 + i) + sy;
+        A.fz[g0 + i] = __ldcg(A.fz + g0 + i) + sz;
       } else {
         A.fx[g0 + i] += sx;
         A.fy[g0 + i] += sy;
@@ -587,6 +595,62 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
   if (BUFFERED)
     for (int lc = threadIdx.x; lc <= nfc; lc += blockDim.x)
       SA.bindex[(int64_t)bid * (SH_MAXF + 1) + lc] = S.fstart[lc];
+}
+
+template <bool ENERGY, int MODE, bool VERLET>
+__global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int colour) {
+  extern __shared__ __align__(16) unsigned char sh_raw[];
+  if constexpr (MODE != SH_DATAFLOW) {
+    shell_block<ENERGY, MODE, VERLET>(SA, sh_raw, colour, blockIdx.x);
+  } else {
+    // Dataflow execution of the colour order: blocks are taken in (colour,
+    // block) order from a ticket; a block starts as soon as its (up to 26)
+    // neighbour blocks of lower colour -- the only ones whose footprints
+    // overlap -- have published, instead of after a global barrier per
+    // colour.  Per particle the contributions still arrive in colour order.
+    __shared__ int s_t;
+    const ForceArgs &A = SA.A;
+    while (true) {
+      if (threadIdx.x == 0) s_t = atomicAdd(SA.ticket, 1);
+      __syncthreads();
+      const int t = s_t;
+      __syncthreads();
+      if (t >= SA.coff[8]) break;
+      int c = 0;
+      while (c < 7 && SA.coff[c + 1] <= t) ++c;
+      const int idx = t - SA.coff[c];
+      const int kc[3] = {c & 1, (c >> 1) & 1, (c >> 2) & 1};
+      const int cnt0 = (A.nbk[0] - kc[0] + 1) >> 1, cnt1 = (A.nbk[1] - kc[1] + 1) >> 1;
+      const int kb[3] = {2 * (idx % cnt0) + kc[0], 2 * ((idx / cnt0) % cnt1) + kc[1],
+                         2 * (idx / (cnt0 * cnt1)) + kc[2]};
+      if (threadIdx.x < 27 && threadIdx.x != 13) {
+        const int d[3] = {(int)threadIdx.x % 3 - 1, ((int)threadIdx.x / 3) % 3 - 1, (int)threadIdx.x / 9 - 1};
+        int nbc[3];
+        bool ok = true;
+        for (int k = 0; k < 3; ++k) {
+          nbc[k] = kb[k] + d[k];
+          if (nbc[k] < 0 || nbc[k] >= A.nbk[k]) {
+            if (A.b.per[k]) nbc[k] = wrap1i(nbc[k], A.nbk[k]);
+            else ok = false;
+          }
+        }
+        if (ok) {
+          const int ncol = (nbc[0] & 1) | ((nbc[1] & 1) << 1) | ((nbc[2] & 1) << 2);
+          if (ncol < c) {
+            const volatile int *f = SA.flags + nbc[0] + A.nbk[0] * (nbc[1] + A.nbk[1] * nbc[2]);
+            while (*f == 0) __nanosleep(64);
+          }
+        }
+        __threadfence();
+      }
+      __syncthreads();
+      shell_block<ENERGY, MODE, VERLET>(SA, sh_raw, c, idx);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0)
+        atomicExch(SA.flags + kb[0] + A.nbk[0] * (kb[1] + A.nbk[1] * kb[2]), 1);
+    }
+  }
 }
 
 // buffered mode: footprint size per block (one warp per block, lanes over cells)
@@ -708,17 +772,20 @@ static size_t shell_buffered_ws(const Box &b, int64_t n) {
 }
 
 typedef void (*ShellKernel)(ShellArgs, int);
-static ShellKernel shell_kernel(bool energy, bool buffered, bool verlet) {
-  static const ShellKernel k[8] = {
-      k_force_shell<false, false, false>, k_force_shell<true, false, false>,
-      k_force_shell<false, true, false>,  k_force_shell<true, true, false>,
-      k_force_shell<false, false, true>,  k_force_shell<true, false, true>,
-      k_force_shell<false, true, true>,   k_force_shell<true, true, true>};
-  return k[(verlet ? 4 : 0) + (buffered ? 2 : 0) + (energy ? 1 : 0)];
+static ShellKernel shell_kernel(bool energy, int mode, bool verlet) {
+  static const ShellKernel k[12] = {
+      k_force_shell<false, 0, false>, k_force_shell<true, 0, false>,
+      k_force_shell<false, 1, false>, k_force_shell<true, 1, false>,
+      k_force_shell<false, 2, false>, k_force_shell<true, 2, false>,
+      k_force_shell<false, 0, true>,  k_force_shell<true, 0, true>,
+      k_force_shell<false, 1, true>,  k_force_shell<true, 1, true>,
+      k_force_shell<false, 2, true>,  k_force_shell<true, 2, true>};
+  return k[(verlet ? 6 : 0) + 2 * mode + (energy ? 1 : 0)];
 }
 
-static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, bool verlet,
+static int launch_shell_passes(const ForceArgs &A, bool energy, int mode, bool verlet,
                                cs_ws *w, int64_t n, unsigned *status, cudaStream_t st) {
+  const bool buffered = mode == SH_BUFFERED;
   const int B[3] = {A.b.blk[0], A.b.blk[1], A.b.blk[2]};
   CS_REQUIRE(B[0] * B[1] * B[2] <= SH_MAXB, "shell schedule: block has more than %d cells", SH_MAXB);
   ShellArgs SA;
@@ -729,14 +796,41 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, bool buffered, b
   const size_t smem = verlet ? sizeof(ShellSmemVL) : sizeof(ShellSmem);
   static bool attr = false;
   if (!attr) {
-    for (int v = 0; v < 8; ++v) {
-      const size_t sm = (v & 4) ? sizeof(ShellSmemVL) : sizeof(ShellSmem);
-      CS_CUDA(cudaFuncSetAttribute(shell_kernel(v & 1, v & 2, v & 4),
+    for (int v = 0; v < 12; ++v) {
+      const bool vl = v >= 6;
+      const size_t sm = vl ? sizeof(ShellSmemVL) : sizeof(ShellSmem);
+      CS_CUDA(cudaFuncSetAttribute(shell_kernel(v & 1, (v % 6) / 2, vl),
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     }
     attr = true;
   }
-  const ShellKernel kern = shell_kernel(energy, buffered, verlet);
+  const ShellKernel kern = shell_kernel(energy, mode, verlet);
+  if (mode == SH_DATAFLOW) {
+    const int64_t nblocks = (int64_t)A.nbk[0] * A.nbk[1] * A.nbk[2];
+    CS_WS_TAKE(*w, int, flags, nblocks + 1);
+    CS_WS_TAKE(*w, unsigned, err, 16);
+    SA.flags = flags;
+    SA.ticket = flags + nblocks;
+    SA.err = status ? status : err;
+    SA.coff[0] = 0;
+    for (int c = 0; c < 8; ++c) {
+      int cnt = 1;
+      for (int k = 0; k < 3; ++k) cnt *= (A.nbk[k] - ((c >> k) & 1) + 1) >> 1;
+      SA.coff[c + 1] = SA.coff[c] + cnt;
+    }
+    static int grid_cap[2] = {0, 0};
+    if (!grid_cap[verlet]) {
+      int per_sm = 0, dev = 0, nsm = 0;
+      CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SH_NW * 32, smem));
+      CS_CUDA(cudaGetDevice(&dev));
+      CS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      grid_cap[verlet] = max(1, per_sm) * nsm;
+    }
+    CS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * (nblocks + 1), st));
+    const unsigned grid = (unsigned)(nblocks < grid_cap[verlet] ? nblocks : grid_cap[verlet]);
+    kern<<<grid, SH_NW * 32, smem, st>>>(SA, -1);
+    return cs_check_launch("force_dataflow");
+  }
   if (buffered) {
     const int64_t nblocks = (int64_t)A.nbk[0] * A.nbk[1] * A.nbk[2];
     CS_WS_TAKE(*w, double, buf, 3 * (8 * n + 64));

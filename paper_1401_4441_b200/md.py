@@ -25,10 +25,14 @@ from .grid import GridSpec
 
 SCHEDULES = {"loopex": _lib.SCHED_LOOPEX, "block": _lib.SCHED_BLOCK, "shell": _lib.SCHED_SHELL,
              "buffered": _lib.SCHED_BUFFERED,
+             # the shell colour order as a dataflow: one persistent launch, each
+             # block waits only for its lower-colour neighbour blocks
+             "dataflow": _lib.SCHED_DATAFLOW,
              # Verlet lists on cells of edge >= rc + skin, under the
-             # buffered or the in-place colour-pass block structure
-             "verlet": _lib.SCHED_BUFFERED, "verlet_shell": _lib.SCHED_SHELL}
-VERLET_SCHEDULES = ("verlet", "verlet_shell")
+             # same block structures
+             "verlet": _lib.SCHED_BUFFERED, "verlet_shell": _lib.SCHED_SHELL,
+             "verlet_dataflow": _lib.SCHED_DATAFLOW}
+VERLET_SCHEDULES = ("verlet", "verlet_shell", "verlet_dataflow")
 
 
 def _torch():
@@ -134,7 +138,7 @@ class LJSystem:
         self.box, self.params, self.n = box, params, int(n)
         self.schedule = schedule
         even = all(c % 2 == 0 for c in box.cells)
-        if schedule in ("shell", "buffered") or self.verlet:
+        if schedule in ("shell", "buffered", "dataflow") or self.verlet:
             self.block = tuple(block) if block is not None else (2, 2, 2)
         elif schedule == "block":
             self.block = tuple(block) if block is not None else choose_block(box.cells)
@@ -418,10 +422,13 @@ class LJSystem:
     def launches_per_step(self, energy: bool = False) -> int:
         """Kernels this package launches per step (memsets excluded)."""
         build = 1 + 3 + 1 + 1  # count, scan x3, scatter, sort-gather
-        if self.verlet:  # kick_drift_track, set_cond, buffered force (sizes, scan x3, force, gather), reduce x2, kick
-            force = (1 + 3 + 1 + 1) if self.schedule == "verlet" else 8
-            return 2 + force + 2 + 1 + (3 if energy else 0)
-        force = (27 if self.schedule == "loopex" else 8) + 2  # passes + pair/energy reduce
+        # force kernels: buffered = block sizes, scan x3, force, gather; shell =
+        # 8 colour passes; dataflow = 1 persistent launch; + pair/energy reduce x2
+        per = {"loopex": 27, "block": 8, "shell": 8, "buffered": 6, "dataflow": 1,
+               "verlet": 6, "verlet_shell": 8, "verlet_dataflow": 1}
+        force = per[self.schedule] + 2
+        if self.verlet:  # kick_drift_track, set_cond (rebuilds run inside the graph's IF node)
+            return 2 + force + 1 + (3 if energy else 0)
         return 1 + build + force + 1 + (3 if energy else 0)
 
     def candidate_pairs(self) -> int:

@@ -35,7 +35,7 @@ def oracle_forces(oracle, sys, snap):
     return f, pe, npair
 
 
-@pytest.mark.parametrize("sched", ["loopex", "block", "shell", "buffered"])
+@pytest.mark.parametrize("sched", ["loopex", "block", "shell", "buffered", "dataflow"])
 def test_cfg1_init_cells_forces(oracle, cuda, sched):
     s = md.LJSystem.fcc(6, schedule=sched)
     assert s.box.cells == (4, 4, 4) and s.n == 864
@@ -60,7 +60,7 @@ def test_cfg1_init_cells_forces(oracle, cuda, sched):
     assert s.pair_count() == npair
 
 
-@pytest.mark.parametrize("sched", ["loopex", "block", "shell", "buffered"])
+@pytest.mark.parametrize("sched", ["loopex", "block", "shell", "buffered", "dataflow"])
 def test_cfg1_trajectory_10_steps(oracle, cuda, sched):
     s = md.LJSystem.fcc(6, schedule=sched)
     ini = {k: v.cpu().numpy()[:864] for k, v in s.initial.items()}
@@ -87,7 +87,7 @@ def test_cfg1_trajectory_10_steps(oracle, cuda, sched):
 def test_forces_vs_oracle_shapes(oracle, cuda, nuc, block):
     box, nucs, a = md.fcc_box(nuc, 0.8442)
     even = all(c % 2 == 0 for c in box.cells)
-    scheds = ["block", "shell", "buffered"] + (["loopex"] if even else [])
+    scheds = ["block", "shell", "buffered", "dataflow"] + (["loopex"] if even else [])
     for sched in scheds:
         try:
             s = md.LJSystem.fcc(nuc, schedule=sched, block=block if sched != "loopex" else None)
@@ -137,6 +137,10 @@ def test_cfg2_full_size_properties(cuda):
     assert force_err(sa["f"], sb["f"]) < FORCE_TOL
     frms = np.sqrt((sa["f"] ** 2).sum(1).mean())
     assert np.abs(sa["f"].sum(0)).max() < 1e-9 * frms * a.n
+    # the dataflow launch adds every block in the same colour order as the
+    # 8 colour passes: bit-identical forces
+    df = md.LJSystem.fcc(48, schedule="dataflow")
+    assert np.array_equal(df.snapshot()["f"], sh.snapshot()["f"])
     # deterministic: same run twice is bit-identical
     c = md.LJSystem.fcc(48, schedule="block")
     assert np.array_equal(c.snapshot()["f"], sa["f"])

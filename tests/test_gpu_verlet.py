@@ -35,7 +35,7 @@ def wrapped_diff(a, b, L):
     return np.abs(d - np.asarray(L) * np.rint(d / np.asarray(L))).max()
 
 
-@pytest.mark.parametrize("sched", ["verlet", "verlet_shell"])
+@pytest.mark.parametrize("sched", ["verlet", "verlet_shell", "verlet_dataflow"])
 def test_verlet_forces_vs_oracle(oracle, cuda, sched):
     s = md.LJSystem.fcc(14, schedule=sched, skin=0.3)
     assert s.box.cells == (8, 8, 8) and s.n == 10976
@@ -49,7 +49,7 @@ def test_verlet_forces_vs_oracle(oracle, cuda, sched):
     assert s.pair_count() == npair
 
 
-@pytest.mark.parametrize("sched", ["verlet", "verlet_shell"])
+@pytest.mark.parametrize("sched", ["verlet", "verlet_shell", "verlet_dataflow"])
 def test_verlet_trajectory_with_rebuilds(oracle, cuda, sched):
     """10 steps with a small skin (several list rebuilds) against the
     oracle's link-cell trajectory from the same initial state."""
@@ -96,6 +96,10 @@ def test_verlet_cfg2_matches_link_cell(cuda):
     fv, fc = by_id(v.snapshot(), "f"), by_id(c.snapshot(), "f")
     assert force_err(fv, fc) < FORCE_TOL
     assert abs(v.energies()[0] - c.energies()[0]) / abs(c.energies()[0]) < ENERGY_TOL
+    # colour passes and their dataflow execution add in the same order
+    vs = md.LJSystem.fcc(48, schedule="verlet_shell", skin=0.3)
+    vd = md.LJSystem.fcc(48, schedule="verlet_dataflow", skin=0.3)
+    assert np.array_equal(vs.snapshot()["f"], vd.snapshot()["f"])
     # deterministic round tables: a second build gives bit-identical forces
     v2 = md.LJSystem.fcc(48, schedule="verlet", skin=0.3)
     assert np.array_equal(v2.snapshot()["f"], v.snapshot()["f"])
