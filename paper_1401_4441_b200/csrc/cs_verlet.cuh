@@ -92,7 +92,7 @@ __device__ __forceinline__ void vl_source(const Box &b, const int32_t *start, in
 
 struct VBuildSmem {
   uint16_t tab[VB_NW][VL_RMAX][32];         // round table of the current cell
-  unsigned long long used[VB_NW][VB_JCAP];  // per candidate j: rounds taken
+  unsigned used[VB_NW][2][VB_JCAP];         // per candidate j: rounds taken (low, high 32)
   unsigned row[VB_NW][32][VB_NCH];          // particle -> candidate bits per chunk
   uint16_t code[VB_NW][VB_JCAP];            // entry << 8 | index in the source cell
   double hx[VB_NW][32][3];                  // home positions (broadcast reads)
@@ -110,8 +110,20 @@ __device__ __forceinline__ int vl_ffs(unsigned v) { return __ffs(v); }
 __device__ __forceinline__ int vl_ffs(unsigned long long v) { return __ffsll((long long)v); }
 
 template <class M>  // round masks: 32 bits while R <= 32, else 64
+__device__ __forceinline__ M vl_used(unsigned (*used)[VB_JCAP], int j);
+template <>
+__device__ __forceinline__ unsigned vl_used<unsigned>(unsigned (*used)[VB_JCAP], int j) {
+  return used[0][j];
+}
+template <>
+__device__ __forceinline__ unsigned long long vl_used<unsigned long long>(unsigned (*used)[VB_JCAP],
+                                                                          int j) {
+  return ((unsigned long long)used[1][j] << 32) | used[0][j];
+}
+
+template <class M>
 __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
-                                         const int *seg_l, unsigned long long *used,
+                                         const int *seg_l, unsigned (*used)[VB_JCAP],
                                          const uint16_t *code, uint16_t (*tab)[32], int lane) {
   bool ok = true;
   int cc = 0;
@@ -126,7 +138,7 @@ __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
     const int jl = cc * 32 + b;
     int r = -1, k = 0;
     if (act) {
-      const M u = (M)used[jl];
+      const M u = vl_used<M>(used, jl);
 #pragma unroll
       for (int kk = VB_SEG - 1; kk >= 0; --kk) {  // first segment with a free round wins
         const M m = fr[kk] & ~u;
@@ -154,7 +166,7 @@ __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
         }
       cur &= ~(1u << b);
       tab[r][tl] = code[jl];
-      atomicOr(&used[jl], 1ull << r);
+      atomicOr(&used[r >> 5][jl], 1u << (r & 31));  // native 32-bit shared atomic
     }
     __syncwarp();
   }
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(VB_NW * 32) k_verlet_build(Box b, const int32_
       // lane -> (first particle, second particle, switch round)
       S.lmap[w][lane] = S.lmap[w][32 + lane] = 0xFF;
       S.lmap[w][64 + lane] = (uint8_t)R;
-      for (int j = lane; j < nj; j += 32) S.used[w][j] = 0ull;
+      for (int j = lane; j < nj; j += 32) S.used[w][0][j] = S.used[w][1][j] = 0u;
       __syncwarp();
       if (lane < na) {
         if (cO != 0) {
