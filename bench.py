@@ -3,9 +3,12 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 A step = one velocity-Verlet step of BASELINE configs[1] (cfg2: FCC 48^3 =
-442,368 particles, rho 0.8442, 32^3 cells, T* 0.722, dt 0.005, fp64):
-kick+drift+wrap, stable counting-sort rebin, LJ half-shell forces with
-Newton-3 reaction writes under the 8-pass colour schedule, kick.
+442,368 particles, rho 0.8442, T* 0.722, dt 0.005, fp64).  Default schedule
+"verlet": kick+drift (+ displacement check), the list rebuild when needed
+(wrap, stable counting-sort rebin, round tables -- inside the CUDA graph as a
+conditional node), LJ half-shell forces with Newton-3 reaction writes under
+the buffered block schedule, kick.  The link-cell kernel (32^3 cells, rebin
+every step) is measured on the same workload and reported alongside.
 `value` = pair interactions per second (pairs within rc per step x steps/s),
 device-timed with CUDA events per step, L2 flushed between steps.
 N > 1 (torchrun): each rank advances its own cfg2-sized block of a
@@ -31,14 +34,18 @@ sys.path.insert(0, ROOT)
 METRIC = "LJ link-cell pair interactions/s (fp64, cfg2 442,368 particles)"
 UNIT = "pair-interactions/s"
 NUC = 48  # cfg2
-WORKLOAD = "cfg2: LJ fluid FCC 48^3 = 442368 particles, rho* 0.8442, T* 0.722, rc 2.5 (unshifted), 32^3 cells, dt 0.005, fp64, 1 VV step"
+WORKLOAD = ("cfg2: LJ fluid FCC 48^3 = 442368 particles, rho* 0.8442, T* 0.722, rc 2.5 (unshifted), "
+            "dt 0.005, fp64, 1 VV step; link cells of edge >= rc (32^3) or, for the Verlet schedules, "
+            ">= rc + skin (28^3)")
 
 
-def traffic_bytes():
-    """DRAM bytes per force launch from the committed ncu --set full capture."""
+def traffic_bytes(schedule):
+    """DRAM bytes per force launch of the schedule's kernel, from the committed
+    ncu --set full capture (profiles/r01_traffic.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            return json.load(f)["dram_bytes_per_launch"]
+            t = json.load(f)
+        return t.get("per_schedule", {}).get(schedule, t.get("dram_bytes_per_launch") if schedule == "buffered" else None)
     except (OSError, KeyError, ValueError):
         return None
 
@@ -221,6 +228,8 @@ def run_slab(args, rank, ws):
     from paper_1401_4441_b200 import _lib, md, slab
 
     dev = torch.cuda.current_device()
+    if args.schedule not in ("shell", "buffered", "dataflow", "block", "loopex"):
+        args.schedule = "buffered"  # the slab engine runs the link-cell kernels
     nuc = (NUC * ws, NUC, NUC)
     box, nucs, a = md.fcc_box(nuc, 0.8442)
     n = 4 * nucs[0] * nucs[1] * nucs[2]
@@ -290,8 +299,51 @@ def run_slab(args, rank, ws):
     print(json.dumps(line), flush=True)
 
 
+def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True):
+    """Graph-replayed VV steps of one schedule, device-timed per phase with CUDA
+    events (L2 flushed before every step).  Returns the system and the timings."""
+    sysm = md.LJSystem.fcc(NUC, schedule=schedule, block=args.block, seed=42 + rank, skin=args.skin)
+    pre, force, post = sysm.graph_phases()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    for _ in range(args.warmup):
+        pre(); force(); post()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    pairs, cands = [], []
+    builds0 = int(sysm.graph_builds.item()) if sysm.verlet else 0
+    barrier(ws)
+    clk = ClockSampler(dev) if clocks else None
+    if clk:
+        clk.__enter__()
+    try:
+        for k in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e = ev[k]
+            e[0].record(); pre(); e[1].record(); force(); e[2].record(); post(); e[3].record()
+            torch.cuda.synchronize()
+            pairs.append(sysm.pair_count())
+            cands.append(sysm.list_pairs() if sysm.verlet else sysm.candidate_pairs())
+    finally:
+        if clk:
+            clk.__exit__(None, None, None)
+    barrier(ws)
+    r = {"sys": sysm, "pairs": pairs, "cands": cands,
+         "step_ms": [e[0].elapsed_time(e[3]) for e in ev],
+         "force_ms": [e[1].elapsed_time(e[2]) for e in ev],
+         "pre_ms": [e[0].elapsed_time(e[1]) for e in ev],
+         "builds": int(sysm.graph_builds.item()) - builds0 if sysm.verlet else None,
+         "clocks": clk.summary() if clk else None}
+    r["tot_s"] = max_over_ranks(sum(r["step_ms"]) * 1e-3, ws)
+    r["value"] = sum_over_ranks(float(sum(pairs)), ws) / r["tot_s"]
+    # roofline of the dominant kernel: algorithmic FLOPs 8 C + 20 P (SURVEY 8d),
+    # C = candidates distance-tested (link-cell half shell, or Verlet list entries)
+    r["achieved"] = sum(8 * c + 20 * p for c, p in zip(cands, pairs)) / (sum(r["force_ms"]) * 1e-3) / 1e12
+    r["achieved_pairs"] = 20 * sum(pairs) / (sum(r["force_ms"]) * 1e-3) / 1e12
+    return r
+
+
 def run_ours(args):
-    import numpy as np
     import torch
 
     rank, ws = dist_init()
@@ -301,39 +353,19 @@ def run_ours(args):
 
     dev = torch.cuda.current_device()
     peak_fp64 = fp64_peak(torch, _lib)
-    sysm = md.LJSystem.fcc(NUC, schedule=args.schedule, block=args.block, seed=42 + rank, skin=args.skin)
-    pre, force, post = sysm.graph_phases()
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
-    for _ in range(args.warmup):
-        pre(); force(); post()
-    torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    pairs, cands = [], []
-    builds0 = int(sysm.graph_builds.item()) if sysm.verlet else 0
-    barrier(ws)
-    with ClockSampler(dev) as clk:
-        for k in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            e = ev[k]
-            e[0].record(); pre(); e[1].record(); force(); e[2].record(); post(); e[3].record()
-            torch.cuda.synchronize()
-            pairs.append(sysm.pair_count())
-            cands.append(sysm.list_pairs() if sysm.verlet else sysm.candidate_pairs())
-    barrier(ws)
-    builds = int(sysm.graph_builds.item()) - builds0 if sysm.verlet else None
-    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
-    force_ms = [e[1].elapsed_time(e[2]) for e in ev]
-    pre_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    tot_s = max_over_ranks(sum(step_ms) * 1e-3, ws)
-    tot_pairs = sum_over_ranks(float(sum(pairs)), ws)
-    value = tot_pairs / tot_s
-    # roofline of the dominant kernel (force passes): algorithmic FLOPs 8C + 20P
-    flops = [8 * c + 20 * p for c, p in zip(cands, pairs)]
-    achieved = sum(flops) / (sum(force_ms) * 1e-3) / 1e12
-    # ---------------------------------------------------------------- e2e
+    m = measure(torch, md, args.schedule, args, args.steps, rank, ws, dev)
+    sysm = m["sys"]
+    # the plain link-cell kernel (no Verlet list) on the same workload, for reference
+    lc = None
+    if sysm.verlet and not args.no_link_cell:
+        ml = measure(torch, md, "buffered", args, min(args.steps, 30), rank, ws, dev, clocks=False)
+        lc = {"schedule": "buffered (2, 2, 2), 32^3 cells", "value": ml["value"],
+              "ms_per_step": 1e3 * ml["tot_s"] / len(ml["step_ms"]),
+              "force_ms_per_step": statistics.mean(ml["force_ms"]),
+              "candidates_per_step": statistics.mean(ml["cands"]),
+              "roofline_frac": ml["achieved"] / peak_fp64, "steps": len(ml["step_ms"])}
+        del ml
     e2e = e2e_run(torch, md, sysm, args)
-    clocks = clk.summary()
     if rank != 0:
         return
     cpu = None
@@ -343,31 +375,41 @@ def run_ours(args):
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{nst} whole cfg2 VV steps in {el:.1f} s (oracle o_md_steps, loop-exchange colour order on OpenMP threads)"}
     n = sysm.n
+    tot_s = m["tot_s"]
+    cfg = {"workload": WORKLOAD, "particles_per_gpu": n, "schedule": f"{args.schedule} {sysm.block}",
+           "cells": list(sysm.box.cells),
+           "l2": "flushed (256 MB memset) between timed steps",
+           "steps_per_s": args.steps / tot_s, "pairs_per_step": statistics.mean(m["pairs"]),
+           "candidates_per_step": statistics.mean(m["cands"]),
+           "force_ms_per_step": statistics.mean(m["force_ms"]),
+           "force_share": sum(m["force_ms"]) / sum(m["step_ms"]),
+           "pre_ms_per_step": statistics.mean(m["pre_ms"]), "pre_ms_median": statistics.median(m["pre_ms"]),
+           "pre_ms_max": max(m["pre_ms"]),
+           "parallelism": f"dp{ws}" if ws > 1 else "single"}
+    if sysm.verlet:
+        cfg.update({"skin": sysm.skin, "list_rebuilds_in_timed_steps": m["builds"],
+                    "verlet": "lists built on the device from the cell list (cells of edge >= rc + skin), "
+                              "rebuilt inside the timed steps by a conditional CUDA-graph node when a "
+                              "particle moved > skin/2; every listed pair re-tested with r^2 < rc^2",
+                    "link_cell_kernel": lc})
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded FCC 48^3 + 0.05 sigma jitter, Gaussian velocities; BASELINE cfg2)",
-        "config": {"workload": WORKLOAD, "particles_per_gpu": n, "schedule": f"{args.schedule} {sysm.block}",
-                   "l2": "flushed (256 MB memset) between timed steps",
-                   "steps_per_s": args.steps / tot_s, "pairs_per_step": statistics.mean(pairs),
-                   "candidates_per_step": statistics.mean(cands),
-                   "force_ms_per_step": statistics.mean(force_ms), "force_share": sum(force_ms) / sum(step_ms),
-                   "pre_ms_per_step": statistics.mean(pre_ms), "pre_ms_max": max(pre_ms),
-                   "pre_ms_median": statistics.median(pre_ms),
-                   "parallelism": f"dp{ws}" if ws > 1 else "single",
-                   **({"skin": sysm.skin, "list_rebuilds_in_timed_steps": builds, "cells": list(sysm.box.cells)}
-                      if sysm.verlet else {})},
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
-                     "frac": achieved / peak_fp64, "traffic": traffic_bytes(),
+        "config": cfg,
+        "roofline": {"bound": "fp64", "achieved": m["achieved"], "peak": peak_fp64, "unit": "TFLOP/s",
+                     "frac": m["achieved"] / peak_fp64, "traffic": traffic_bytes(args.schedule),
                      "kernel": f"k_force_shell ({args.schedule} schedule)",
-                     "flops_convention": "8 C + 20 P per force evaluation (SURVEY 8d)",
+                     "flops_convention": "8 C + 20 P per force evaluation (SURVEY 8d); C = pairs distance-tested",
+                     "achieved_pair_flops": m["achieved_pairs"],
+                     "frac_pair_flops": m["achieved_pairs"] / peak_fp64,
                      "peak_source": "measured live: cs_probe_dfma DFMA chains (MEASURED_PEAKS.json has no FP64 entry)",
                      "hbm_peak_gbs": peaks().get("hbm_gbs")},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps * sysm.launches_per_step(),
-        "clocks": clocks,
+        "clocks": m["clocks"],
     }
     print(json.dumps(line), flush=True)
 
@@ -409,7 +451,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--schedule", default="buffered",
+    ap.add_argument("--no-link-cell", action="store_true", help="skip the link-cell comparison run")
+    ap.add_argument("--schedule", default="verlet",
                     choices=["shell", "buffered", "dataflow", "block", "loopex", "verlet", "verlet_shell",
                              "verlet_dataflow"])
     ap.add_argument("--skin", type=float, default=0.3, help="Verlet skin (verlet schedules)")

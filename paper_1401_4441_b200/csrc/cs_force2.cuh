@@ -53,12 +53,11 @@ struct MergeTable {              // host-built per block shape
 template <int RCAP_, int HCAP_>
 struct ShellBase {
   static constexpr int RCAP = RCAP_, HCAP = HCAP_;
-  double R[3][RCAP];                 // reaction slots (e >= 1)
-  double Fh[3][HCAP];                // home rows (e = 0)
+  double RF[3][RCAP + HCAP];         // reaction slots (e >= 1), then home rows (e = 0)
   double sh[SH_MAXB][16][3];         // image shift of source (h, e); e = 15: idle
   int sstart[SH_MAXB][16];           // global start of source (h, e)
   int scount[SH_MAXB][16];           // count of source (h, e), -1: none
-  int sbase[SH_MAXB][16];            // slot base (Fh for e = 0, R for e >= 1)
+  int sbase[SH_MAXB][16];            // slot base in RF (home rows for e = 0)
   int fstart[SH_MAXF + 1];           // footprint cell -> offset in the block buffer
   int fgstart[SH_MAXF];              // footprint cell -> global start (-1: none)
   int hcell[SH_MAXB];
@@ -97,7 +96,7 @@ __device__ __forceinline__ int wrap1i(int v, int n) { return v < 0 ? v + n : (v 
 // that round (no atomics).  Every listed pair is re-tested exactly
 // (r^2 < rc^2).  Descriptors are prefetched two rounds ahead and partner
 // positions one round ahead (the image shift is added when used).
-template <bool ENERGY, class SM>
+template <bool ENERGY, bool SHIFT, class SM>
 __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, int a0,
                                              const uint16_t *dp, int nr, int pA, int pB, int sw,
                                              double *fa, double *fb, double &pe,
@@ -116,10 +115,11 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, i
     zb = __ldg(A.z + a0 + pB);
   }
   double fx_ = 0, fy_ = 0, fz_ = 0;
-  // idle slots are entry 15: a real particle shifted 1e150 away (no branch)
+  // descriptors two rounds ahead, partner positions one round ahead; idle
+  // slots (entry 15) point at a real particle and never pass the r^2 test
   unsigned d0 = nr > 0 ? __ldg(dp) : VL_IDLE;
   unsigned d1 = nr > 1 ? __ldg(dp + 32) : VL_IDLE;
-  int g0 = S.sstart[h][d0 >> 8] + (d0 & 255);
+  const int g0 = S.sstart[h][d0 >> 8] + (d0 & 255);
   double x0 = __ldg(A.x + g0), y0 = __ldg(A.y + g0), z0 = __ldg(A.z + g0);
   dp += 64;
   for (int r = 0; r < nr; ++r) {
@@ -138,9 +138,18 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, i
     const double x1 = __ldg(A.x + g1), y1 = __ldg(A.y + g1), z1 = __ldg(A.z + g1);
     {
       const int e = d0 >> 8;
-      const double dx = xi - (x0 + S.sh[h][e][0]), dy = yi - (y0 + S.sh[h][e][1]),
-                   dz = zi - (z0 + S.sh[h][e][2]);
-      const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+      double dx, dy, dz;
+      if (SHIFT) {  // home cell at a periodic face: image shift per entry (entry 15: 1e150)
+        dx = xi - (x0 + S.sh[h][e][0]);
+        dy = yi - (y0 + S.sh[h][e][1]);
+        dz = zi - (z0 + S.sh[h][e][2]);
+      } else {
+        dx = xi - x0;
+        dy = yi - y0;
+        dz = zi - z0;
+      }
+      double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+      if (!SHIFT && e == 15) r2 = 1e300;
       if (r2 < rc2) {
         const double ri = fast_rcp(r2);
         const double s2 = sig2 * ri;
@@ -150,9 +159,8 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, i
         fx_ += fx;
         fy_ += fy;
         fz_ += fz;
-        const int slot = S.sbase[h][e] + (d0 & 255);
-        double *dst = e == 0 ? &S.Fh[0][slot] : &S.R[0][slot];
-        const int stride = e == 0 ? HCAP : RCAP;
+        double *dst = &S.RF[0][S.sbase[h][e] + (d0 & 255)];
+        constexpr int stride = RCAP + HCAP;
         dst[0] -= fx;
         dst[stride] -= fy;
         dst[2 * stride] -= fz;
@@ -198,9 +206,9 @@ __device__ __forceinline__ void verlet_fi(SM &S, int h, int lane, int im, double
   const int prev = __shfl_up_sync(CS_FULL, im, 1);
   if (im != 0xFF && (lane == 0 || prev != im)) {
     const int slot = S.sbase[h][0] + im;
-    S.Fh[0][slot] += fix;
-    S.Fh[1][slot] += fiy;
-    S.Fh[2][slot] += fiz;
+    S.RF[0][slot] += fix;
+    S.RF[1][slot] += fiy;
+    S.RF[2][slot] += fiz;
   }
   __syncwarp();
 }
@@ -217,8 +225,14 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
     double pe = 0;
     unsigned hits = 0;
     double fa[3] = {0, 0, 0}, fb[3] = {0, 0, 0};
-    verlet_table<ENERGY>(S, A, h, S.sstart[h][0], A.vl_desc + (int64_t)cell * (VL_RMAX * 32) + lane,
-                         nr, pA, pB, sw, fa, fb, pe, hits);
+    const uint16_t *dp = A.vl_desc + (int64_t)cell * (VL_RMAX * 32) + lane;
+    const bool shift = __any_sync(CS_FULL, lane < 14 && (S.sh[h][lane < 14 ? lane : 0][0] != 0.0 ||
+                                                         S.sh[h][lane < 14 ? lane : 0][1] != 0.0 ||
+                                                         S.sh[h][lane < 14 ? lane : 0][2] != 0.0));
+    if (shift)
+      verlet_table<ENERGY, true>(S, A, h, S.sstart[h][0], dp, nr, pA, pB, sw, fa, fb, pe, hits);
+    else
+      verlet_table<ENERGY, false>(S, A, h, S.sstart[h][0], dp, nr, pA, pB, sw, fa, fb, pe, hits);
     verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2]);
     verlet_fi(S, h, lane, pB, fb[0], fb[1], fb[2]);
     hits = warp_sum(hits);
@@ -336,7 +350,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
         const int vh = __shfl_up_sync(CS_FULL, ih, s), vr = __shfl_up_sync(CS_FULL, ir, s);
         if (lane >= s) { ih += vh; ir += vr; }
       }
-      if (t < nhome * 14) S.sbase[h][e] = e == 0 ? fb + ih - ch : rb + ir - cr;
+      if (t < nhome * 14) S.sbase[h][e] = e == 0 ? RCAP + fb + ih - ch : rb + ir - cr;
       fb += __shfl_sync(CS_FULL, ih, 31);
       rb += __shfl_sync(CS_FULL, ir, 31);
     }
@@ -393,8 +407,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     return;
     }
   }
-  for (int i = threadIdx.x; i < RCAP; i += blockDim.x) S.R[0][i] = S.R[1][i] = S.R[2][i] = 0.0;
-  for (int i = threadIdx.x; i < HCAP; i += blockDim.x) S.Fh[0][i] = S.Fh[1][i] = S.Fh[2][i] = 0.0;
+  for (int i = threadIdx.x; i < RCAP + HCAP; i += blockDim.x) S.RF[0][i] = S.RF[1][i] = S.RF[2][i] = 0.0;
   __syncthreads();
 
   const double edge0 = b.L[0] / b.gnc[0], edge1 = b.L[1] / b.gnc[1], edge2 = b.L[2] / b.gnc[2];
@@ -518,9 +531,8 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
           }
         }
         if (vj) {  // unique writer of slot (h, e, q)
-          const int slot = S.sbase[h][e] + q;
-          double *dst = e == 0 ? &S.Fh[0][slot] : &S.R[0][slot];
-          const int stride = e == 0 ? HCAP : RCAP;
+          double *dst = &S.RF[0][S.sbase[h][e] + q];
+          constexpr int stride = RCAP + HCAP;
           dst[0] += gx;
           dst[stride] += gy;
           dst[2 * stride] += gz;
@@ -538,7 +550,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
             s2 += S.rows[wid][q][c][l + 2];
             s3 += S.rows[wid][q][c][l + 3];
           }
-          S.Fh[c][fh0 + ib + q] += (s0 + s1) + (s2 + s3);
+          S.RF[c][fh0 + ib + q] += (s0 + s1) + (s2 + s3);
         }
       }
       __syncwarp();
@@ -552,44 +564,42 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   }
   }  // link-cell super-tasks
   __syncthreads();
-  // ---- 5. merge per footprint cell in a fixed order
+  // ---- 5. merge, one thread per footprint particle: home rows + reaction
+  //         slots in the fixed merge-table order
   const int64_t boff = BUFFERED ? SA.boff[bid] : 0;
-  for (int lc = wid; lc < nfc; lc += SH_NW) {
+  const int nfoot = S.fstart[nfc];
+  for (int t = threadIdx.x; t < nfoot; t += blockDim.x) {
+    int lc = 0;  // footprint cell: last lc with fstart[lc] <= t
+#pragma unroll
+    for (int k = 32; k >= 1; k >>= 1)
+      if (lc + k < nfc && S.fstart[lc + k] <= t) lc += k;
     const int g0 = S.fgstart[lc];
     if (g0 < 0) continue;
-    const int n = S.fstart[lc + 1] - S.fstart[lc];
+    const int i = t - S.fstart[lc];
     const int nc = SA.mt.n[lc];
-    for (int i = lane; i < n; i += 32) {
-      double sx = 0, sy = 0, sz = 0;
-      for (int k = 0; k < nc; ++k) {
-        const int he = SA.mt.he[lc][k];
-        const int hh = he >> 4, e = he & 15;
-        if (S.hcell[hh] < 0) continue;
-        const int s = S.sbase[hh][e] + i;
-        if (e == 0) {
-          sx += S.Fh[0][s];
-          sy += S.Fh[1][s];
-          sz += S.Fh[2][s];
-        } else {
-          sx += S.R[0][s];
-          sy += S.R[1][s];
-          sz += S.R[2][s];
-        }
-      }
-      if (BUFFERED) {
-        const int64_t o = boff + S.fstart[lc] + i;
-        SA.buf[o] = sx;
-        SA.buf[SA.bufstride + o] = sy;
-        SA.buf[2 * SA.bufstride + o] = sz;
-      } else if (MODE == SH_DATAFLOW) {  // other SMs wrote f: read through L2
-        A.fx[g0 + i] = __ldcg(A.fx + g0 + i) + sx;
-        A.fy[g0 + i] = __ldcg(A.fy + g0 + i) + sy;
-        A.fz[g0 + i] = __ldcg(A.fz + g0 + i) + sz;
-      } else {
-        A.fx[g0 + i] += sx;
-        A.fy[g0 + i] += sy;
-        A.fz[g0 + i] += sz;
-      }
+    double sx = 0, sy = 0, sz = 0;
+    for (int k = 0; k < nc; ++k) {
+      const int he = SA.mt.he[lc][k];
+      const int hh = he >> 4, e = he & 15;
+      if (S.hcell[hh] < 0) continue;
+      const int s = S.sbase[hh][e] + i;
+      sx += S.RF[0][s];
+      sy += S.RF[1][s];
+      sz += S.RF[2][s];
+    }
+    if (BUFFERED) {
+      const int64_t o = boff + t;
+      SA.buf[o] = sx;
+      SA.buf[SA.bufstride + o] = sy;
+      SA.buf[2 * SA.bufstride + o] = sz;
+    } else if (MODE == SH_DATAFLOW) {  // other SMs wrote f: read through L2
+      A.fx[g0 + i] = __ldcg(A.fx + g0 + i) + sx;
+      A.fy[g0 + i] = __ldcg(A.fy + g0 + i) + sy;
+      A.fz[g0 + i] = __ldcg(A.fz + g0 + i) + sz;
+    } else {
+      A.fx[g0 + i] += sx;
+      A.fy[g0 + i] += sy;
+      A.fz[g0 + i] += sz;
     }
   }
   if (BUFFERED)
