@@ -455,7 +455,7 @@ def main():
     ap.add_argument("--schedule", default="verlet",
                     choices=["shell", "buffered", "dataflow", "block", "loopex", "verlet", "verlet_shell",
                              "verlet_dataflow"])
-    ap.add_argument("--skin", type=float, default=0.3, help="Verlet skin (verlet schedules)")
+    ap.add_argument("--skin", type=float, default=0.35, help="Verlet skin (verlet schedules)")
     ap.add_argument("--block", type=lambda s: tuple(int(v) for v in s.split(",")), default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true", help="use the x-slab engine even at N=1")

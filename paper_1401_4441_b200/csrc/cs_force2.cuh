@@ -96,13 +96,62 @@ __device__ __forceinline__ int wrap1i(int v, int n) { return v < 0 ? v + n : (v 
 // that round (no atomics).  Every listed pair is re-tested exactly
 // (r^2 < rc^2).  Descriptors are prefetched two rounds ahead and partner
 // positions one round ahead (the image shift is added when used).
+// one listed pair of round-table descriptor d with partner position (xj, yj,
+// zj) (unshifted): returns the force on i (0 if idle or r >= rc)
+template <bool ENERGY, bool SHIFT, class SM>
+__device__ __forceinline__ bool verlet_pair(SM &S, const ForceArgs &A, int h, unsigned d,
+                                            double xi, double yi, double zi, double xj, double yj,
+                                            double zj, double &fx, double &fy, double &fz,
+                                            double &pe) {
+  const int e = d >> 8;
+  double dx, dy, dz;
+  if (SHIFT) {  // home cell at a periodic face: image shift per entry (entry 15: 1e150)
+    dx = xi - (xj + S.sh[h][e][0]);
+    dy = yi - (yj + S.sh[h][e][1]);
+    dz = zi - (zj + S.sh[h][e][2]);
+  } else {
+    dx = xi - xj;
+    dy = yi - yj;
+    dz = zi - zj;
+  }
+  double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+  if (!SHIFT && e == 15) r2 = 1e300;
+  const bool hit = r2 < A.p.rc2;
+  fx = fy = fz = 0.0;
+  if (hit) {
+    const double ri = fast_rcp(r2);
+    const double s2 = A.p.sig2 * ri;
+    const double s6 = s2 * s2 * s2;
+    const double ff = A.p.eps48 * s6 * (s6 - 0.5) * ri;
+    fx = ff * dx;
+    fy = ff * dy;
+    fz = ff * dz;
+    if (ENERGY) pe += A.p.eps4 * s6 * (s6 - 1.0);
+  }
+  return hit;
+}
+
+// Newton-3 reaction of a hit into the (h, e) slot of j: no other lane writes
+// this slot in this round
+template <class SM>
+__device__ __forceinline__ void verlet_react(SM &S, int h, unsigned d, double fx, double fy,
+                                             double fz) {
+  constexpr int stride = SM::RCAP + SM::HCAP;
+  double *dst = &S.RF[0][S.sbase[h][d >> 8] + (d & 255)];
+  dst[0] -= fx;
+  dst[stride] -= fy;
+  dst[2 * stride] -= fz;
+}
+
+// Rounds are taken in pairs (the builder aligns switch rounds to even): the
+// two pairs of a lane are independent chains (ILP); their reactions are
+// written round by round, each round's j being distinct.  Descriptors are
+// prefetched two rounds ahead of the pair being computed, positions one.
 template <bool ENERGY, bool SHIFT, class SM>
 __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, int a0,
                                              const uint16_t *dp, int nr, int pA, int pB, int sw,
                                              double *fa, double *fb, double &pe,
                                              unsigned &hits) {
-  constexpr int RCAP = SM::RCAP, HCAP = SM::HCAP;
-  const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
   double xi = 0, yi = 0, zi = 0, xb = 0, yb = 0, zb = 0;
   if (pA != 0xFF) {
     xi = __ldg(A.x + a0 + pA);
@@ -115,14 +164,15 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, i
     zb = __ldg(A.z + a0 + pB);
   }
   double fx_ = 0, fy_ = 0, fz_ = 0;
-  // descriptors two rounds ahead, partner positions one round ahead; idle
-  // slots (entry 15) point at a real particle and never pass the r^2 test
-  unsigned d0 = nr > 0 ? __ldg(dp) : VL_IDLE;
-  unsigned d1 = nr > 1 ? __ldg(dp + 32) : VL_IDLE;
-  const int g0 = S.sstart[h][d0 >> 8] + (d0 & 255);
-  double x0 = __ldg(A.x + g0), y0 = __ldg(A.y + g0), z0 = __ldg(A.z + g0);
-  dp += 64;
-  for (int r = 0; r < nr; ++r) {
+  // idle slots (entry 15) read a real particle and never pass the r^2 test
+  unsigned d0 = nr > 0 ? __ldg(dp) : VL_IDLE, d1 = nr > 1 ? __ldg(dp + 32) : VL_IDLE;
+  unsigned d2 = nr > 2 ? __ldg(dp + 64) : VL_IDLE, d3 = nr > 3 ? __ldg(dp + 96) : VL_IDLE;
+  int g = S.sstart[h][d0 >> 8] + (d0 & 255);
+  double x0 = __ldg(A.x + g), y0 = __ldg(A.y + g), z0 = __ldg(A.z + g);
+  g = S.sstart[h][d1 >> 8] + (d1 & 255);
+  double x1 = __ldg(A.x + g), y1 = __ldg(A.y + g), z1 = __ldg(A.z + g);
+  dp += 128;
+  for (int r = 0; r < nr; r += 2) {
     if (r == sw) {  // this lane continues with its second particle
       fa[0] = fx_;
       fa[1] = fy_;
@@ -132,48 +182,34 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, i
       yi = yb;
       zi = zb;
     }
-    const unsigned d2 = r + 2 < nr ? __ldg(dp) : VL_IDLE;
-    dp += 32;
-    const int g1 = S.sstart[h][d1 >> 8] + (d1 & 255);
-    const double x1 = __ldg(A.x + g1), y1 = __ldg(A.y + g1), z1 = __ldg(A.z + g1);
-    {
-      const int e = d0 >> 8;
-      double dx, dy, dz;
-      if (SHIFT) {  // home cell at a periodic face: image shift per entry (entry 15: 1e150)
-        dx = xi - (x0 + S.sh[h][e][0]);
-        dy = yi - (y0 + S.sh[h][e][1]);
-        dz = zi - (z0 + S.sh[h][e][2]);
-      } else {
-        dx = xi - x0;
-        dy = yi - y0;
-        dz = zi - z0;
-      }
-      double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
-      if (!SHIFT && e == 15) r2 = 1e300;
-      if (r2 < rc2) {
-        const double ri = fast_rcp(r2);
-        const double s2 = sig2 * ri;
-        const double s6 = s2 * s2 * s2;
-        const double ff = eps48 * s6 * (s6 - 0.5) * ri;
-        const double fx = ff * dx, fy = ff * dy, fz = ff * dz;
-        fx_ += fx;
-        fy_ += fy;
-        fz_ += fz;
-        double *dst = &S.RF[0][S.sbase[h][e] + (d0 & 255)];
-        constexpr int stride = RCAP + HCAP;
-        dst[0] -= fx;
-        dst[stride] -= fy;
-        dst[2 * stride] -= fz;
-        if (ENERGY) pe += eps4 * s6 * (s6 - 1.0);
-        ++hits;
-      }
-    }
-    d0 = d1;
-    d1 = d2;
-    x0 = x1;
-    y0 = y1;
-    z0 = z1;
+    const unsigned d4 = r + 4 < nr ? __ldg(dp) : VL_IDLE;
+    const unsigned d5 = r + 5 < nr ? __ldg(dp + 32) : VL_IDLE;
+    dp += 64;
+    g = S.sstart[h][d2 >> 8] + (d2 & 255);
+    const double x2 = __ldg(A.x + g), y2 = __ldg(A.y + g), z2 = __ldg(A.z + g);
+    g = S.sstart[h][d3 >> 8] + (d3 & 255);
+    const double x3 = __ldg(A.x + g), y3 = __ldg(A.y + g), z3 = __ldg(A.z + g);
+    double ux, uy, uz, vx, vy, vz;
+    const bool h0 = verlet_pair<ENERGY, SHIFT>(S, A, h, d0, xi, yi, zi, x0, y0, z0, ux, uy, uz, pe);
+    const bool h1 = verlet_pair<ENERGY, SHIFT>(S, A, h, d1, xi, yi, zi, x1, y1, z1, vx, vy, vz, pe);
+    fx_ += ux + vx;
+    fy_ += uy + vy;
+    fz_ += uz + vz;
+    hits += (unsigned)h0 + (unsigned)h1;
+    if (h0) verlet_react(S, h, d0, ux, uy, uz);
     __syncwarp();
+    if (h1) verlet_react(S, h, d1, vx, vy, vz);
+    __syncwarp();
+    d0 = d2;
+    d1 = d3;
+    d2 = d4;
+    d3 = d5;
+    x0 = x2;
+    y0 = y2;
+    z0 = z2;
+    x1 = x3;
+    y1 = y3;
+    z1 = z3;
   }
   if (sw < nr) {
     fb[0] = fx_;

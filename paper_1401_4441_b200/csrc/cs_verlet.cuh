@@ -267,6 +267,12 @@ __global__ void __launch_bounds__(VB_NW * 32) k_verlet_build(Box b, const int32_
           ++Lc;
           off = segs = 0;
         }
+        if (off & 1) {  // switch rounds are even: the force kernel takes rounds in pairs
+          if (++off == R) {
+            ++Lc;
+            off = segs = 0;
+          }
+        }
         if (lane == p) {
           cL = Lc;
           cO = off;

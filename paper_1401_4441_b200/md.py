@@ -221,6 +221,10 @@ class LJSystem:
         Verlet schedules bin on cells of edge >= rc + skin."""
         verlet = schedule in VERLET_SCHEDULES
         box, nuc, a = fcc_box(n_unit_cells, density, params.rc + (skin if verlet else 0.0))
+        if verlet and any(c % 4 for c in box.cells):
+            # the 2x2x2 block colouring needs multiples of 4 cells: widen the cells
+            cells = tuple(max(4, c - c % 4) for c in box.cells)
+            box = LJBox(box.lengths, cells)
         n = 4 * nuc[0] * nuc[1] * nuc[2]
         s = cls(box, n, params, schedule, block, skin=skin)
         s.dt = dt
