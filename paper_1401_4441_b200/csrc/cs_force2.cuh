@@ -604,11 +604,18 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   //         slots in the fixed merge-table order
   const int64_t boff = BUFFERED ? SA.boff[bid] : 0;
   const int nfoot = S.fstart[nfc];
-  for (int t = threadIdx.x; t < nfoot; t += blockDim.x) {
-    int lc = 0;  // footprint cell: last lc with fstart[lc] <= t
+  const bool all_homes = __syncthreads_and(threadIdx.x >= nhome || S.hcell[threadIdx.x] >= 0);
+  for (int t0 = wid * 32; t0 < nfoot; t0 += blockDim.x) {
+    int lc = 0;  // footprint cell of t0 (lane 0), then step forward per lane
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 32; k >= 1; k >>= 1)
-      if (lc + k < nfc && S.fstart[lc + k] <= t) lc += k;
+      for (int k = 32; k >= 1; k >>= 1)
+        if (lc + k < nfc && S.fstart[lc + k] <= t0) lc += k;
+    }
+    lc = __shfl_sync(CS_FULL, lc, 0);
+    const int t = t0 + lane;
+    if (t >= nfoot) continue;
+    while (lc + 1 < nfc && S.fstart[lc + 1] <= t) ++lc;
     const int g0 = S.fgstart[lc];
     if (g0 < 0) continue;
     const int i = t - S.fstart[lc];
@@ -617,7 +624,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     for (int k = 0; k < nc; ++k) {
       const int he = SA.mt.he[lc][k];
       const int hh = he >> 4, e = he & 15;
-      if (S.hcell[hh] < 0) continue;
+      if (!all_homes && S.hcell[hh] < 0) continue;  // (slab ranks: homes past the owned planes)
       const int s = S.sbase[hh][e] + i;
       sx += S.RF[0][s];
       sy += S.RF[1][s];
