@@ -32,6 +32,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "LJ link-cell pair interactions/s (fp64, cfg2 442,368 particles)"
+METRIC_CFG5 = "LJ link-cell pair interactions/s (fp64, cfg5 liquid-vapour slab, 3,486,176 particles)"
+WORKLOAD_CFG5 = ("cfg5: periodic 64x64x192 cells of edge 2.5 (160x160x480); FCC liquid (rho 0.811, the cubic "
+                 "lattice tiling 160 closest to 0.8) in the middle third along z, uniform vapour rho 0.02 "
+                 "elsewhere with no pair closer than 0.9; T* 0.85, rc 2.5, dt 0.005, fp64, 1 VV step")
 UNIT = "pair-interactions/s"
 NUC = 48  # cfg2
 WORKLOAD = ("cfg2: LJ fluid FCC 48^3 = 442368 particles, rho* 0.8442, T* 0.722, rc 2.5 (unshifted), "
@@ -142,11 +146,19 @@ def barrier(ws):
 
 
 # --------------------------------------------------------------- CPU arms --
-def cpu_setup(nthreads):
+def cpu_setup(nthreads, config="cfg2"):
     import numpy as np
 
     from oracle import oracle as O
 
+    if config == "cfg5":
+        from paper_1401_4441_b200.md import liquid_vapour_positions
+
+        L, xyz = liquid_vapour_positions()
+        n = len(xyz)
+        vx, vy, vz = O.velocities(n, 0.85, 1.0, 42)
+        return O.CpuMD(*(np.ascontiguousarray(xyz[:, k]) for k in range(3)), vx, vy, vz,
+                       np.arange(n, dtype=np.int32), [64, 64, 192], list(L), nthreads=nthreads)
     rho = 0.8442
     a = (4 / rho) ** (1 / 3)
     L = NUC * a
@@ -156,9 +168,9 @@ def cpu_setup(nthreads):
     return O.CpuMD(x, y, z, vx, vy, vz, np.arange(n, dtype=np.int32), [32] * 3, [L] * 3, nthreads=nthreads)
 
 
-def cpu_sample(nthreads, min_seconds=10.0, max_steps=200):
-    """Bounded sample: whole cfg2 steps until >= min_seconds of CPU work."""
-    m = cpu_setup(nthreads)
+def cpu_sample(nthreads, min_seconds=10.0, max_steps=200, config="cfg2"):
+    """Bounded sample: whole steps until >= min_seconds of CPU work."""
+    m = cpu_setup(nthreads, config)
     steps, pairs, t0 = 0, 0, time.perf_counter()
     while True:
         _, _, npairs = m.steps(1)
@@ -176,7 +188,7 @@ def run_reference(args):
     import numpy as np
 
     cores = len(os.sched_getaffinity(0))
-    m = cpu_setup(cores)
+    m = cpu_setup(cores, args.config)
     for _ in range(args.warmup):
         m.steps(1)
     times, pairs = [], 0
@@ -188,14 +200,16 @@ def run_reference(args):
     tot = sum(times)
     value = pairs / tot
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC_CFG5 if args.config == "cfg5" else METRIC, "value": value,
+        "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded FCC + jitter, Gaussian velocities)",
-        "config": {"workload": WORKLOAD, "schedule": "loop-exchange colour order, 27 levels, OpenMP over tasks of a level",
+        "config": {"workload": WORKLOAD_CFG5 if args.config == "cfg5" else WORKLOAD,
+                   "schedule": "loop-exchange colour order, 27 levels, OpenMP over tasks of a level",
                    "steps_per_s": args.steps / tot},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} whole cfg2 VV steps (oracle/cs_oracle.c o_md_steps)"},
+                         "sample": f"{args.steps} whole {args.config} VV steps (oracle/cs_oracle.c o_md_steps)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -302,7 +316,10 @@ def run_slab(args, rank, ws):
 def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True):
     """Graph-replayed VV steps of one schedule, device-timed per phase with CUDA
     events (L2 flushed before every step).  Returns the system and the timings."""
-    sysm = md.LJSystem.fcc(NUC, schedule=schedule, block=args.block, seed=42 + rank, skin=args.skin)
+    if args.config == "cfg5":
+        sysm = md.LJSystem.liquid_vapour(schedule=schedule, block=args.block, seed=42 + rank, skin=args.skin)
+    else:
+        sysm = md.LJSystem.fcc(NUC, schedule=schedule, block=args.block, seed=42 + rank, skin=args.skin)
     pre, force, post = sysm.graph_phases()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(args.warmup):
@@ -357,7 +374,7 @@ def run_ours(args):
     sysm = m["sys"]
     # the plain link-cell kernel (no Verlet list) on the same workload, for reference
     lc = None
-    if sysm.verlet and not args.no_link_cell:
+    if sysm.verlet and not args.no_link_cell and args.config == "cfg2":
         ml = measure(torch, md, "buffered", args, min(args.steps, 30), rank, ws, dev, clocks=False)
         lc = {"schedule": "buffered (2, 2, 2), 32^3 cells", "value": ml["value"],
               "ms_per_step": 1e3 * ml["tot_s"] / len(ml["step_ms"]),
@@ -371,12 +388,12 @@ def run_ours(args):
     cpu = None
     if ws == 1 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
-        v, nst, el = cpu_sample(cores, min_seconds=args.cpu_seconds)
+        v, nst, el = cpu_sample(cores, min_seconds=args.cpu_seconds, config=args.config)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{nst} whole cfg2 VV steps in {el:.1f} s (oracle o_md_steps, loop-exchange colour order on OpenMP threads)"}
+               "sample": f"{nst} whole {args.config} VV steps in {el:.1f} s (oracle o_md_steps, loop-exchange colour order on OpenMP threads)"}
     n = sysm.n
     tot_s = m["tot_s"]
-    cfg = {"workload": WORKLOAD, "particles_per_gpu": n, "schedule": f"{args.schedule} {sysm.block}",
+    cfg = {"workload": WORKLOAD_CFG5 if args.config == "cfg5" else WORKLOAD, "particles_per_gpu": n, "schedule": f"{args.schedule} {sysm.block}",
            "cells": list(sysm.box.cells),
            "l2": "flushed (256 MB memset) between timed steps",
            "steps_per_s": args.steps / tot_s, "pairs_per_step": statistics.mean(m["pairs"]),
@@ -393,10 +410,13 @@ def run_ours(args):
                               "particle moved > skin/2; every listed pair re-tested with r^2 < rc^2",
                     "link_cell_kernel": lc})
     line = {
-        "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": METRIC_CFG5 if args.config == "cfg5" else METRIC, "value": m["value"], "unit": UNIT,
+        "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded FCC 48^3 + 0.05 sigma jitter, Gaussian velocities; BASELINE cfg2)",
+        "data": ("synthetic (seeded liquid slab + rejection-sampled vapour, Gaussian velocities; BASELINE cfg5)"
+                 if args.config == "cfg5" else
+                 "synthetic (seeded FCC 48^3 + 0.05 sigma jitter, Gaussian velocities; BASELINE cfg2)"),
         "config": cfg,
         "roofline": {"bound": "fp64", "achieved": m["achieved"], "peak": peak_fp64, "unit": "TFLOP/s",
                      "frac": m["achieved"] / peak_fp64, "traffic": traffic_bytes(args.schedule),
@@ -452,6 +472,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-link-cell", action="store_true", help="skip the link-cell comparison run")
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg5"],
+                    help="BASELINE workload: cfg2 (headline) or cfg5 (liquid-vapour load-imbalance stress)")
     ap.add_argument("--schedule", default="verlet",
                     choices=["shell", "buffered", "dataflow", "block", "loopex", "verlet", "verlet_shell",
                              "verlet_dataflow"])

@@ -102,6 +102,57 @@ def fcc_box(n_unit_cells, density: float, rc: float = 2.5):
     return LJBox.for_cutoff(lengths, rc), nuc, (a, a, a)
 
 
+def liquid_vapour_positions(cells=(64, 64, 192), edge: float = 2.5, rho_liquid: float = 0.8,
+                            rho_vapour: float = 0.02, rmin: float = 0.9, seed: int = 42):
+    """BASELINE configs[4] (cfg5): a periodic box of cells x edge; the middle
+    third along z holds an FCC liquid, the rest a uniform-random vapour with
+    no pair closer than rmin.  Host set-up (numpy + scipy's periodic KD-tree),
+    deterministic in `seed`.  Returns (lengths, xyz[n, 3]); liquid first.
+
+    The liquid is a cubic FCC lattice that tiles x and y exactly, with the
+    number of unit cells closest to rho_liquid (cfg5: 94 per 160 sigma, density
+    0.811), filling 94 unit cells of the middle third along z.  Vapour
+    candidates are drawn in batches; one closer than rmin to the liquid, to an
+    accepted vapour particle or to an earlier candidate of its batch is
+    redrawn (a deterministic batch form of rejection sampling)."""
+    import numpy as np
+    from scipy.spatial import cKDTree
+
+    L = np.asarray(cells, np.float64) * edge
+    if abs(L[0] - L[1]) > 1e-12:
+        raise ValueError("the liquid lattice needs equal x and y extents")
+    a0 = (4.0 / rho_liquid) ** (1.0 / 3.0)
+    nx = max(1, int(round(L[0] / a0)))
+    a = L[0] / nx
+    nz = max(1, min(int(round(L[2] / 3.0 / a)), int(L[2] // a)))
+    z0 = (L[2] - nz * a) / 2.0
+    ii, jj, kk = np.meshgrid(np.arange(nx), np.arange(nx), np.arange(nz), indexing="ij")
+    basis = np.array([[0, 0, 0], [0, 0.5, 0.5], [0.5, 0, 0.5], [0.5, 0.5, 0]])
+    cell = np.stack([ii.ravel(), jj.ravel(), kk.ravel()], 1).astype(np.float64)
+    liquid = ((cell[:, None, :] + basis[None, :, :] + 0.25) * a).reshape(-1, 3)
+    liquid[:, 2] += z0
+    vap_h = L[2] - nz * a
+    nv = int(round(rho_vapour * L[0] * L[1] * vap_h))
+    rng = np.random.default_rng(seed)
+    tree_l = cKDTree(liquid, boxsize=L)
+    vap = np.zeros((0, 3))
+    while len(vap) < nv:
+        cand = rng.random((nv - len(vap), 3)) * np.array([L[0], L[1], vap_h])
+        cand[:, 2] = np.where(cand[:, 2] < z0, cand[:, 2], cand[:, 2] + nz * a)
+        cand = np.mod(cand, L)
+        ok = tree_l.query(cand, distance_upper_bound=rmin)[0] >= rmin
+        if len(vap):
+            ok &= cKDTree(vap, boxsize=L).query(cand, distance_upper_bound=rmin)[0] >= rmin
+        bad = set()
+        for i, j in sorted(cKDTree(cand, boxsize=L).query_pairs(rmin)):
+            if i not in bad:
+                bad.add(j)
+        if bad:
+            ok[sorted(bad)] = False
+        vap = np.concatenate([vap, cand[ok]])
+    return tuple(float(v) for v in L), np.concatenate([liquid, vap])
+
+
 def choose_block(cells, density_per_cell: float = 13.5, cap: int = 2048):
     """Largest block (By, Bz >= 2) whose 2x2x2 colour passes still fill the
     GPU (>= 296 CTAs per pass) and whose footprint fits the staging cap."""
@@ -230,6 +281,38 @@ class LJSystem:
         s.dt = dt
         s.seed_fcc(nuc, a, temperature, jitter, seed)
         return s
+
+    @classmethod
+    def liquid_vapour(cls, cells=(64, 64, 192), edge: float = 2.5, temperature: float = 0.85,
+                      seed: int = 42, params: LJParams = LJParams(), schedule: str = "buffered",
+                      block=None, dt: float = 0.005, skin: float = 0.3, **kw):
+        """cfg5 (BASELINE configs[4]): liquid slab + vapour (liquid_vapour_positions),
+        Gaussian velocities at T on the device.  Link-cell schedules bin on the
+        given cells (edge = rc for cfg5); Verlet schedules on cells of edge
+        >= rc + skin (multiples of 4)."""
+        L, xyz = liquid_vapour_positions(cells, edge, seed=seed, **kw)
+        verlet = schedule in VERLET_SCHEDULES
+        box = LJBox(L, cells)
+        if verlet:
+            box = LJBox.for_cutoff(L, params.rc + skin)
+            box = LJBox(L, tuple(max(4, c - c % 4) for c in box.cells))
+        s = cls(box, len(xyz), params, schedule, block, skin=skin)
+        s.dt = dt
+        s.seed_positions(xyz, temperature, seed)
+        return s
+
+    def seed_positions(self, xyz, temperature, seed):
+        """Host positions (ids = row order) + device Gaussian velocities at T."""
+        torch = _torch()
+        b = self._buf[self.cur]
+        for k, col in zip(("x", "y", "z"), range(3)):
+            b[k][: self.n].copy_(torch.as_tensor(xyz[:, col], dtype=torch.float64))
+        b["id"][: self.n].copy_(torch.arange(self.n, dtype=torch.int32))
+        _lib.call("cs_init_velocities", self.n, float(temperature), self.params.mass, int(seed),
+                  _lib.ptr(b["vx"]), _lib.ptr(b["vy"]), _lib.ptr(b["vz"]), _lib.ptr(self._ws),
+                  self._wsb, self._s())
+        self.initial = {k: b[k].clone() for k in ("x", "y", "z", "vx", "vy", "vz", "id")}
+        self.rebuild()
 
     def seed_fcc(self, nuc, a, temperature, jitter, seed):
         src = self.cur
