@@ -217,9 +217,12 @@ class LJSystem:
                   L.cs_reduce_ws_bytes(self.n))
         self._wsb = int(wsb)
         self._ws = torch.empty(self._wsb, dtype=torch.uint8, device=d)
-        self.scal = torch.zeros(8, dtype=f64, device=d)  # [0]=PE [1]=KE
-        self.npairs = torch.zeros(1, dtype=torch.int64, device=d)
-        self.status = torch.zeros(1, dtype=torch.int32, device=d)  # kernel capacity flags
+        # step results in one device block, read back with one copy (readout)
+        self._out = torch.zeros(80, dtype=torch.uint8, device=d)
+        self.scal = self._out[0:64].view(f64)  # [0]=PE [1]=KE
+        self.npairs = self._out[64:72].view(torch.int64)
+        self.status = self._out[72:76].view(torch.int32)  # kernel capacity flags
+        self._out_host = torch.empty(80, dtype=torch.uint8).pin_memory()
         self.dt = 0.005
         self._graphs = {}
         self._capturing = False
@@ -584,6 +587,20 @@ class LJSystem:
         if st & 4:
             raise _lib.CellschedError("Verlet list: a home cell needs more than 64 rounds; "
                                       "reduce the skin")
+
+    def readout(self):
+        """(PE, KE, pairs) of the last step with one device->host copy and one
+        synchronisation (raises on a kernel capacity flag)."""
+        import numpy as np
+
+        torch = _torch()
+        self._out_host.copy_(self._out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        raw = self._out_host.numpy()
+        if int(raw[72:76].view(np.int32)[0]):
+            self.check_status()
+        e = raw[0:16].view(np.float64)
+        return float(e[0]), float(e[1]), int(raw[64:72].view(np.int64)[0])
 
     def energies(self):
         """(PE, KE) of the last energy evaluation (synchronises)."""
