@@ -40,6 +40,7 @@ struct ForceArgs {
   const int32_t *vl_nround;
   const uint8_t *vl_imap;
   const uint16_t *vl_desc;
+  const int32_t *vl_boff;  // buffered block offsets computed at the list build
 };
 
 // level (0..26) -> (stencil entry, parity); level 0 = intra

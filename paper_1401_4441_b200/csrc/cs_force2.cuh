@@ -899,8 +899,12 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, int mode, bool v
     SA.bindex = bindex;
     SA.bufstride = 8 * n + 64;
     SA.err = status ? status : err;
-    k_block_sizes<<<grid_for(nblocks * 32, 256), 256, 0, st>>>(SA, sizes);
-    CS_TRY(cs_exclusive_scan_i32(sizes, boff, nblocks, scratch, sb, st));
+    if (A.vl_boff) {  // Verlet mode: the layout was computed at the list build
+      SA.boff = A.vl_boff;
+    } else {
+      k_block_sizes<<<grid_for(nblocks * 32, 256), 256, 0, st>>>(SA, sizes);
+      CS_TRY(cs_exclusive_scan_i32(sizes, boff, nblocks, scratch, sb, st));
+    }
     kern<<<(unsigned)nblocks, SH_NW * 32, smem, st>>>(SA, -1);
     const int64_t ncell = (int64_t)A.b.nc[0] * A.b.nc[1] * A.b.nc[2];
     k_gather_blocks<<<(unsigned)((ncell * 32 + 255) / 256), 256, 0, st>>>(SA);

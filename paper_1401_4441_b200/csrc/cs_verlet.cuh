@@ -33,11 +33,15 @@ struct VList {
   int32_t *nround;  // rounds R of the cell's table
   uint8_t *imap;    // [cell][96]: lane -> first particle, second particle, switch round
   uint16_t *desc;   // [cell][VL_RMAX][32]
+  int32_t *bsizes;  // buffered block layout (fixed between rebuilds): footprint sizes,
+  int32_t *boff;    //   their exclusive scan = block buffer offsets
+  void *scan_ws;    //   scan scratch
 };
 
-static size_t vl_bytes(int64_t ncell) {
+static size_t vl_bytes(int64_t ncell) {  // (blocks <= cells bounds the layout arrays)
   return cs_ws_slice(sizeof(int32_t) * ncell) + cs_ws_slice(96 * (size_t)ncell) +
-         cs_ws_slice(sizeof(uint16_t) * (size_t)VL_RMAX * 32 * ncell);
+         cs_ws_slice(sizeof(uint16_t) * (size_t)VL_RMAX * 32 * ncell) +
+         2 * cs_ws_slice(sizeof(int32_t) * (ncell + 2)) + cs_ws_slice(cs_scan_ws_bytes(ncell + 1));
 }
 
 static VList vl_view(void *p, int64_t ncell) {
@@ -48,6 +52,12 @@ static VList vl_view(void *p, int64_t ncell) {
   v.imap = (uint8_t *)c;
   c += cs_ws_slice(96 * (size_t)ncell);
   v.desc = (uint16_t *)c;
+  c += cs_ws_slice(sizeof(uint16_t) * (size_t)VL_RMAX * 32 * ncell);
+  v.bsizes = (int32_t *)c;
+  c += cs_ws_slice(sizeof(int32_t) * (ncell + 2));
+  v.boff = (int32_t *)c;
+  c += cs_ws_slice(sizeof(int32_t) * (ncell + 2));
+  v.scan_ws = c;
   return v;
 }
 
@@ -56,6 +66,7 @@ static void vl_attach(ForceArgs &A, const void *vlist) {
   A.vl_nround = v.nround;
   A.vl_imap = v.imap;
   A.vl_desc = v.desc;
+  A.vl_boff = v.boff;
 }
 
 extern "C" size_t cs_verlet_list_bytes(const cs_box *bx) {
@@ -460,6 +471,23 @@ extern "C" int cs_verlet_build(const cs_box *bx, const cs_lj *lj, double skin,
   }
   if (blocks > 0)
     k_verlet_build<<<(unsigned)blocks, VB_NW * 32, 0, st>>>(b, cell_start, x, y, z, rl2, L, status_dev);
+  // the buffered block layout only changes with the cell list: compute it here
+  // once per rebuild instead of in every force evaluation
+  int nbk[3];
+  if (block_grid(b, nbk) == CS_OK) {
+    ShellArgs SA;
+    memset(&SA, 0, sizeof(SA));
+    SA.A.b = b;
+    SA.A.start = cell_start;
+    for (int k = 0; k < 3; ++k) SA.A.nbk[k] = nbk[k];
+    const int B[3] = {b.blk[0], b.blk[1], b.blk[2]};
+    if (b.blk[0] * b.blk[1] * b.blk[2] <= SH_MAXB && build_merge_table(B, &SA.mt) == CS_OK) {
+      const int64_t nblocks = (int64_t)nbk[0] * nbk[1] * nbk[2];
+      k_block_sizes<<<grid_for(nblocks * 32, 256), 256, 0, st>>>(SA, L.bsizes);
+      CS_TRY(cs_exclusive_scan_i32(L.bsizes, L.boff, nblocks, L.scan_ws,
+                                   cs_scan_ws_bytes(b.ncells + 1), st));
+    }
+  }
   if (x0 && n > 0) k_copy3<<<grid_for(n, 256), 256, 0, st>>>(n, x, y, z, x0, y0, z0);
   return cs_check_launch("verlet_build");
 }

@@ -515,7 +515,7 @@ class LJSystem:
         # force kernels: buffered = block sizes, scan x3, force, gather; shell =
         # 8 colour passes; dataflow = 1 persistent launch; + pair/energy reduce x2
         per = {"loopex": 27, "block": 8, "shell": 8, "buffered": 6, "dataflow": 1,
-               "verlet": 6, "verlet_shell": 8, "verlet_dataflow": 1}
+               "verlet": 2, "verlet_shell": 8, "verlet_dataflow": 1}  # verlet: layout cached at build
         force = per[self.schedule] + 2
         if self.verlet:  # kick_drift_track, set_cond (rebuilds run inside the graph's IF node)
             return 2 + force + 1 + (3 if energy else 0)
