@@ -41,6 +41,7 @@ struct ForceArgs {
   const uint8_t *vl_imap;
   const uint16_t *vl_desc;
   const int32_t *vl_boff;  // buffered block offsets computed at the list build
+  const unsigned char *vl_tab;  // per-block tables computed at the list build
 };
 
 // level (0..26) -> (stencil entry, parity); level 0 = intra

@@ -293,6 +293,7 @@ struct ShellArgs {
   int *flags;             // dataflow mode: per block "published" flag
   int *ticket;            // dataflow mode: next (colour, block) ticket
   int coff[9];            // dataflow mode: first ticket of each colour
+  const unsigned char *vtab;  // Verlet mode: per-block tables cached at the list build
 };
 
 // block coordinates -> global cell of a footprint cell (or -1)
@@ -305,34 +306,20 @@ __device__ __forceinline__ int64_t foot_cell(const Box &b, const int *o0, int lc
 }
 
 
-template <bool ENERGY, int MODE, bool VERLET>
-__device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *sh_raw, int colour,
-                                            int bid) {
-  constexpr bool BUFFERED = MODE == SH_BUFFERED;
-  using SM = typename std::conditional<VERLET, ShellSmemVL, ShellSmem>::type;
+// Phase 0 of a block: source tables per (home h, entry e), slot bases,
+// footprint offsets and the capacity flag, in shared memory.  Depends only on
+// the cell list (cached per block at a Verlet list build).
+template <bool VERLET, class SM>
+__device__ __forceinline__ void shell_tables(const ShellArgs &SA, SM &S, const int *o0) {
   constexpr int RCAP = SM::RCAP, HCAP = SM::HCAP;
-  SM &S = *reinterpret_cast<SM *>(sh_raw);
   const ForceArgs &A = SA.A;
   const Box &b = A.b;
   const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
   const int nhome = B0 * B1 * B2;
-  int o0[3];
-  if (BUFFERED) {
-    o0[0] = (bid % A.nbk[0]) * B0;
-    o0[1] = ((bid / A.nbk[0]) % A.nbk[1]) * B1;
-    o0[2] = (bid / (A.nbk[0] * A.nbk[1])) * B2;
-  } else {
-    const int kc0 = colour & 1, kc1 = (colour >> 1) & 1, kc2 = (colour >> 2) & 1;
-    const int cnt0 = (A.nbk[0] - kc0 + 1) >> 1, cnt1 = (A.nbk[1] - kc1 + 1) >> 1;
-    o0[0] = (2 * (bid % cnt0) + kc0) * B0;
-    o0[1] = (2 * ((bid / cnt0) % cnt1) + kc1) * B1;
-    o0[2] = (2 * (bid / (cnt0 * cnt1)) + kc2) * B2;
-  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int FX = B0 + 1, FY = B1 + 2;
   const int nfc = SA.mt.nfc;
-
-  // ---- 0. source tables, one thread per (h, e); footprint cells
+  // source tables, one thread per (h, e); footprint cells
   for (int t = threadIdx.x; t < nhome * 14; t += blockDim.x) {
     const int h = t / 14, e = t - 14 * h;
     const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
@@ -414,6 +401,51 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     }
   }
   __syncthreads();
+}
+
+// bytes of the cached per-block tables: ShellBase from `sh` through `overflow`
+__host__ __device__ constexpr size_t vl_table_bytes() {
+  return (offsetof(ShellSmemVL, overflow) + sizeof(int) - offsetof(ShellSmemVL, sh) + 15) & ~(size_t)15;
+}
+
+template <bool ENERGY, int MODE, bool VERLET>
+__device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *sh_raw, int colour,
+                                            int bid) {
+  constexpr bool BUFFERED = MODE == SH_BUFFERED;
+  using SM = typename std::conditional<VERLET, ShellSmemVL, ShellSmem>::type;
+  constexpr int RCAP = SM::RCAP, HCAP = SM::HCAP;
+  SM &S = *reinterpret_cast<SM *>(sh_raw);
+  const ForceArgs &A = SA.A;
+  const Box &b = A.b;
+  const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
+  const int nhome = B0 * B1 * B2;
+  int o0[3];
+  if (BUFFERED) {
+    o0[0] = (bid % A.nbk[0]) * B0;
+    o0[1] = ((bid / A.nbk[0]) % A.nbk[1]) * B1;
+    o0[2] = (bid / (A.nbk[0] * A.nbk[1])) * B2;
+  } else {
+    const int kc0 = colour & 1, kc1 = (colour >> 1) & 1, kc2 = (colour >> 2) & 1;
+    const int cnt0 = (A.nbk[0] - kc0 + 1) >> 1, cnt1 = (A.nbk[1] - kc1 + 1) >> 1;
+    o0[0] = (2 * (bid % cnt0) + kc0) * B0;
+    o0[1] = (2 * ((bid / cnt0) % cnt1) + kc1) * B1;
+    o0[2] = (2 * (bid / (cnt0 * cnt1)) + kc2) * B2;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nfc = SA.mt.nfc;
+
+  bool cached = false;
+  if constexpr (VERLET) {
+    if (SA.vtab) {  // tables cached at the list build: 16-byte copy into shared memory
+      const int blin = o0[0] / B0 + A.nbk[0] * (o0[1] / B1 + A.nbk[1] * (o0[2] / B2));
+      const int4 *src = reinterpret_cast<const int4 *>(SA.vtab + (size_t)blin * vl_table_bytes());
+      int4 *dst = reinterpret_cast<int4 *>(reinterpret_cast<unsigned char *>(&S) + offsetof(SM, sh));
+      for (int k = threadIdx.x; k < (int)(vl_table_bytes() / 16); k += blockDim.x) dst[k] = __ldg(src + k);
+      __syncthreads();
+      cached = true;
+    }
+  }
+  if (!cached) shell_tables<VERLET>(SA, S, o0);
   if (S.overflow) {
     if constexpr (MODE != SH_COLOUR) {  // no in-place fallback: report to the host
       if (threadIdx.x == 0) atomicExch(SA.err, 1u);
@@ -706,6 +738,22 @@ __global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int
   }
 }
 
+// Verlet list build: the per-block tables of every block (buffered block
+// order), cached for the force evaluations until the next build.  Shared
+// memory holds only the table part of ShellSmemVL.
+__global__ void __launch_bounds__(SH_NW * 32) k_vl_tables(ShellArgs SA, unsigned char *out) {
+  extern __shared__ __align__(16) unsigned char sh_raw[];
+  ShellSmemVL &S = *reinterpret_cast<ShellSmemVL *>(sh_raw - offsetof(ShellSmemVL, sh));
+  const ForceArgs &A = SA.A;
+  const int bid = blockIdx.x;
+  const int o0[3] = {(bid % A.nbk[0]) * A.b.blk[0], ((bid / A.nbk[0]) % A.nbk[1]) * A.b.blk[1],
+                     (bid / (A.nbk[0] * A.nbk[1])) * A.b.blk[2]};
+  shell_tables<true>(SA, S, o0);
+  const int4 *src = reinterpret_cast<const int4 *>(sh_raw);
+  int4 *dst = reinterpret_cast<int4 *>(out + (size_t)bid * vl_table_bytes());
+  for (int k = threadIdx.x; k < (int)(vl_table_bytes() / 16); k += blockDim.x) dst[k] = src[k];
+}
+
 // buffered mode: footprint size per block (one warp per block, lanes over cells)
 __global__ void k_block_sizes(ShellArgs SA, int32_t *sizes) {
   const ForceArgs &A = SA.A;
@@ -845,6 +893,7 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, int mode, bool v
   memset(&SA, 0, sizeof(SA));
   SA.A = A;
   SA.overwrite = verlet ? 1 : 0;
+  SA.vtab = A.vl_tab;
   CS_TRY(build_merge_table(B, &SA.mt));
   const size_t smem = verlet ? sizeof(ShellSmemVL) : sizeof(ShellSmem);
   static bool attr = false;

@@ -36,12 +36,20 @@ struct VList {
   int32_t *bsizes;  // buffered block layout (fixed between rebuilds): footprint sizes,
   int32_t *boff;    //   their exclusive scan = block buffer offsets
   void *scan_ws;    //   scan scratch
+  unsigned char *tab;  // per-block force-kernel tables (vl_table_bytes each)
 };
 
-static size_t vl_bytes(int64_t ncell) {  // (blocks <= cells bounds the layout arrays)
+static int64_t vl_blocks(const Box &b) {
+  const int B0 = b.blk[0] > 0 ? b.blk[0] : 1, B1 = b.blk[1] > 0 ? b.blk[1] : 1, B2 = b.blk[2] > 0 ? b.blk[2] : 1;
+  return (int64_t)((b.owned_x + B0 - 1) / B0) * ((b.nc[1] + B1 - 1) / B1) * ((b.nc[2] + B2 - 1) / B2);
+}
+
+static size_t vl_bytes(const Box &b) {  // (blocks <= cells bounds the layout arrays)
+  const int64_t ncell = b.ncells;
   return cs_ws_slice(sizeof(int32_t) * ncell) + cs_ws_slice(96 * (size_t)ncell) +
          cs_ws_slice(sizeof(uint16_t) * (size_t)VL_RMAX * 32 * ncell) +
-         2 * cs_ws_slice(sizeof(int32_t) * (ncell + 2)) + cs_ws_slice(cs_scan_ws_bytes(ncell + 1));
+         2 * cs_ws_slice(sizeof(int32_t) * (ncell + 2)) + cs_ws_slice(cs_scan_ws_bytes(ncell + 1)) +
+         cs_ws_slice(vl_table_bytes() * (size_t)vl_blocks(b));
 }
 
 static VList vl_view(void *p, int64_t ncell) {
@@ -58,6 +66,8 @@ static VList vl_view(void *p, int64_t ncell) {
   v.boff = (int32_t *)c;
   c += cs_ws_slice(sizeof(int32_t) * (ncell + 2));
   v.scan_ws = c;
+  c += cs_ws_slice(cs_scan_ws_bytes(ncell + 1));
+  v.tab = (unsigned char *)c;
   return v;
 }
 
@@ -67,12 +77,13 @@ static void vl_attach(ForceArgs &A, const void *vlist) {
   A.vl_imap = v.imap;
   A.vl_desc = v.desc;
   A.vl_boff = v.boff;
+  A.vl_tab = v.tab;
 }
 
 extern "C" size_t cs_verlet_list_bytes(const cs_box *bx) {
   Box b;
   if (make_box(bx, &b) != CS_OK) return 0;
-  return vl_bytes(b.ncells);
+  return vl_bytes(b);
 }
 
 // source cell of stencil entry e for home cell (h0, h1, h2): start, count
@@ -458,8 +469,8 @@ extern "C" int cs_verlet_build(const cs_box *bx, const cs_lj *lj, double skin,
                "cell edge %.6g on axis %d is below rc + skin = %.6g", b.L[k] / b.gnc[k], k,
                lj->rc + skin);
   }
-  CS_REQUIRE(list_bytes >= vl_bytes(b.ncells), "Verlet list buffer too small (%zu < %zu)",
-             list_bytes, vl_bytes(b.ncells));
+  CS_REQUIRE(list_bytes >= vl_bytes(b), "Verlet list buffer too small (%zu < %zu)",
+             list_bytes, vl_bytes(b));
   CS_REQUIRE(status_dev, "status pointer required");
   VList L = vl_view(list, b.ncells);
   const double rl = lj->rc + skin;
@@ -486,6 +497,7 @@ extern "C" int cs_verlet_build(const cs_box *bx, const cs_lj *lj, double skin,
       k_block_sizes<<<grid_for(nblocks * 32, 256), 256, 0, st>>>(SA, L.bsizes);
       CS_TRY(cs_exclusive_scan_i32(L.bsizes, L.boff, nblocks, L.scan_ws,
                                    cs_scan_ws_bytes(b.ncells + 1), st));
+      k_vl_tables<<<(unsigned)nblocks, SH_NW * 32, vl_table_bytes(), st>>>(SA, L.tab);
     }
   }
   if (x0 && n > 0) k_copy3<<<grid_for(n, 256), 256, 0, st>>>(n, x, y, z, x0, y0, z0);
