@@ -326,24 +326,28 @@ def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True):
         pre(); force(); post()
     torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
-    pairs, cands = [], []
+    # per-step counts stay on the device (no host synchronisation inside the
+    # loop, so host launch latency is not timed); they are read at the end
+    hist = torch.zeros((2, steps), dtype=torch.int64, device="cuda")
     builds0 = int(sysm.graph_builds.item()) if sysm.verlet else 0
     barrier(ws)
+    torch.cuda.synchronize()
     clk = ClockSampler(dev) if clocks else None
     if clk:
         clk.__enter__()
     try:
         for k in range(steps):
-            flush.zero_()
-            torch.cuda.synchronize()
+            flush.zero_()  # L2 flush between timed steps (outside e[0]..e[3])
             e = ev[k]
             e[0].record(); pre(); e[1].record(); force(); e[2].record(); post(); e[3].record()
-            torch.cuda.synchronize()
-            pairs.append(sysm.pair_count())
-            cands.append(sysm.list_pairs() if sysm.verlet else sysm.candidate_pairs())
+            hist[0, k].copy_(sysm.npairs[0])
+            hist[1, k].copy_(sysm.list_pairs_dev() if sysm.verlet else sysm.candidate_pairs_dev())
+        torch.cuda.synchronize()
     finally:
         if clk:
             clk.__exit__(None, None, None)
+    sysm.check_status()
+    pairs, cands = hist[0].tolist(), hist[1].tolist()
     barrier(ws)
     r = {"sys": sysm, "pairs": pairs, "cands": cands,
          "step_ms": [e[0].elapsed_time(e[3]) for e in ev],

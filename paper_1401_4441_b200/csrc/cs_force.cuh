@@ -42,6 +42,9 @@ struct ForceArgs {
   const uint16_t *vl_desc;
   const int32_t *vl_boff;  // buffered block offsets computed at the list build
   const unsigned char *vl_tab;  // per-block tables computed at the list build
+  // super-task kernels: pair counts added straight into the total (integer
+  // atomics, order-independent), so non-energy steps need no reduction pass
+  unsigned long long *npairs_direct;
 };
 
 // level (0..26) -> (stencil entry, parity); level 0 = intra
@@ -126,11 +129,13 @@ __device__ __forceinline__ void task_warp(const double *__restrict__ x,
 
 template <bool ENERGY>
 __device__ __forceinline__ void task_stats(double pe, unsigned hits, int64_t home,
-                                           double *pe_cell, unsigned *hits_cell) {
+                                           double *pe_cell, unsigned *hits_cell,
+                                           unsigned long long *npairs_direct = nullptr) {
   hits = warp_sum(hits);
   if (ENERGY) pe = warp_sum(pe);
   if ((threadIdx.x & 31) == 0) {
-    hits_cell[home] += hits;
+    if (npairs_direct) atomicAdd(npairs_direct, (unsigned long long)hits);
+    else hits_cell[home] += hits;
     if (ENERGY) pe_cell[home] += pe;
   }
 }
@@ -425,7 +430,10 @@ static int lj_forces_impl(const cs_box *bx, const cs_lj *lj, int sched, int64_t 
   A.hits_cell = hits_cell;
   const bool energy = energy_dev != nullptr;
   if (energy) CS_CUDA(cudaMemsetAsync(pe_cell, 0, sizeof(double) * nc, st));
-  CS_CUDA(cudaMemsetAsync(hits_cell, 0, sizeof(unsigned) * nc, st));
+  const bool direct = vlist || sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED ||
+                      sched == CS_SCHED_DATAFLOW;
+  A.npairs_direct = direct ? npairs_dev : nullptr;
+  if (!direct) CS_CUDA(cudaMemsetAsync(hits_cell, 0, sizeof(unsigned) * nc, st));
   if (vlist) {
     CS_REQUIRE(sched == CS_SCHED_SHELL || sched == CS_SCHED_BUFFERED || sched == CS_SCHED_DATAFLOW,
                "Verlet forces run under CS_SCHED_SHELL, CS_SCHED_BUFFERED or CS_SCHED_DATAFLOW");
@@ -480,10 +488,11 @@ static int lj_forces_impl(const cs_box *bx, const cs_lj *lj, int sched, int64_t 
     CS_REQUIRE(0, "unknown schedule %d", sched);
   }
   CS_TRY(cs_check_launch("lj_forces"));
-  if (energy || npairs_dev) {
+  if (energy || (npairs_dev && !direct)) {
+    if (direct) CS_CUDA(cudaMemsetAsync(hits_cell, 0, sizeof(unsigned) * nc, st));  // (unused)
     int np = (int)cs_reduce_partials(nc);
     k_reduce_cells<<<np, RED_THREADS, 0, st>>>(nc, pe_cell, hits_cell, part, hpart, energy);
-    k_reduce_cells_final<<<1, 1024, 0, st>>>(np, part, hpart, energy_dev, npairs_dev);
+    k_reduce_cells_final<<<1, 1024, 0, st>>>(np, part, hpart, energy_dev, direct ? nullptr : npairs_dev);
   }
   return cs_check_launch("lj_forces_reduce");
 }

@@ -274,7 +274,8 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
     hits = warp_sum(hits);
     if (ENERGY) pe = warp_sum(pe);
     if (lane == 0) {
-      A.hits_cell[cell] += hits;
+      if (A.npairs_direct) atomicAdd(A.npairs_direct, (unsigned long long)hits);
+      else A.hits_cell[cell] += hits;
       if (ENERGY) A.pe_cell[cell] += pe;
     }
     __syncwarp();
@@ -468,7 +469,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
         task_warp<ENERGY>(A.x, A.y, A.z, a0, na, b0, nb, level == 0, S.sh[h][e][0], S.sh[h][e][1],
                           S.sh[h][e][2], A.fx + a0, A.fy + a0, A.fz + a0, A.fx + b0, A.fy + b0,
                           A.fz + b0, A.p, pe, hits);
-        task_stats<ENERGY>(pe, hits, S.hcell[h], A.pe_cell, A.hits_cell);
+        task_stats<ENERGY>(pe, hits, S.hcell[h], A.pe_cell, A.hits_cell, A.npairs_direct);
       }
       __syncthreads();
     }
@@ -626,7 +627,8 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     hits = warp_sum(hits);
     if (ENERGY) pe = warp_sum(pe);
     if (lane == 0) {
-      A.hits_cell[S.hcell[h]] += hits;
+      if (A.npairs_direct) atomicAdd(A.npairs_direct, (unsigned long long)hits);
+      else A.hits_cell[S.hcell[h]] += hits;
       if (ENERGY) A.pe_cell[S.hcell[h]] += pe;
     }
   }

@@ -516,29 +516,31 @@ class LJSystem:
         # 8 colour passes; dataflow = 1 persistent launch; + pair/energy reduce x2
         per = {"loopex": 27, "block": 8, "shell": 8, "buffered": 6, "dataflow": 1,
                "verlet": 2, "verlet_shell": 8, "verlet_dataflow": 1}  # verlet: layout cached at build
-        force = per[self.schedule] + 2
+        direct = self.schedule not in ("loopex", "block")  # pair counts via atomics in the kernel
+        force = per[self.schedule] + (2 if (energy or not direct) else 0)
         if self.verlet:  # kick_drift_track, set_cond (rebuilds run inside the graph's IF node)
             return 2 + force + 1 + (3 if energy else 0)
         return 1 + build + force + 1 + (3 if energy else 0)
 
-    def candidate_pairs(self) -> int:
-        """Half-shell candidate pairs C of the current cell list (the
-        algorithmic-FLOP convention 8 C + 20 P of SURVEY 8(d))."""
-        import numpy as np
-
-        cnt = np.diff(self.cell_start.cpu().numpy()).astype(np.int64).reshape(self.box.cells[::-1])
-        c = int((cnt * (cnt - 1) // 2).sum())
+    def candidate_pairs_dev(self):
+        """Half-shell candidate pairs C of the current cell list as a device
+        scalar (no synchronisation): the C of the 8 C + 20 P convention of
+        SURVEY 8(d) for the link-cell schedules."""
+        torch = _torch()
         from .grid import canonical_half_stencil
 
-        for off in canonical_half_stencil(3).inter_offsets:
-            ox, oy, oz = off
-            nb = np.roll(cnt, shift=(-oz, -oy, -ox), axis=(0, 1, 2))
-            c += int((cnt * nb).sum())
+        cnt = (self.cell_start[1:] - self.cell_start[:-1]).long().view(*self.box.cells[::-1])
+        c = (cnt * (cnt - 1) // 2).sum()
+        for ox, oy, oz in canonical_half_stencil(3).inter_offsets:
+            c = c + (cnt * torch.roll(cnt, shifts=(-oz, -oy, -ox), dims=(0, 1, 2))).sum()
         return c
 
-    def list_pairs(self) -> int:
-        """Verlet mode: pairs held in the current round tables (each is
-        distance-tested every step; the C of the 8 C + 20 P convention)."""
+    def candidate_pairs(self) -> int:
+        return int(self.candidate_pairs_dev())
+
+    def list_pairs_dev(self):
+        """Verlet mode: pairs held in the current round tables, as a device
+        scalar (each is distance-tested every step)."""
         torch = _torch()
         nc = self.box.cell_count
         sl = lambda b: (b + 255) // 256 * 256  # cs_ws_slice, layout of vl_view
@@ -546,7 +548,10 @@ class LJSystem:
         nr = self.vlist[: 4 * nc].view(torch.int32).long()
         desc = self.vlist[o2: o2 + 2 * 64 * 32 * nc].view(torch.int16).view(nc, 64, 32)
         live = torch.arange(64, device=self.device)[None, :] < nr[:, None]
-        return int(((desc != 0x0F00) & live[:, :, None]).sum())  # VL_IDLE
+        return ((desc != 0x0F00) & live[:, :, None]).sum()  # VL_IDLE
+
+    def list_pairs(self) -> int:
+        return int(self.list_pairs_dev())
 
     def list_rounds(self):
         """Verlet mode: (rounds per cell as a host array, lane use)."""
