@@ -62,6 +62,8 @@ struct ShellBase {
   int fgstart[SH_MAXF];              // footprint cell -> global start (-1: none)
   int hcell[SH_MAXB];
   int overflow;
+  uint8_t mt_n[SH_MAXF];           // merge table in shared memory: lanes of one warp read
+  uint8_t mt_he[SH_MAXF][SH_MAXC];  //   different cells (divergent constant reads serialise)
 };
 struct ShellSmem : ShellBase<SH_RCAP, SH_HCAP> {  // link-cell super-tasks
   double rows[SH_NW][SH_IB][3][32];  // per-lane i partials
@@ -447,6 +449,13 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     }
   }
   if (!cached) shell_tables<VERLET>(SA, S, o0);
+  // merge table into shared memory (after the table copy, which may write
+  // up to 15 padding bytes past `overflow`); read after later barriers
+  for (int k = threadIdx.x; k < SH_MAXF; k += blockDim.x) {
+    S.mt_n[k] = SA.mt.n[k];
+#pragma unroll
+    for (int c = 0; c < SH_MAXC; ++c) S.mt_he[k][c] = SA.mt.he[k][c];
+  }
   if (S.overflow) {
     if constexpr (MODE != SH_COLOUR) {  // no in-place fallback: report to the host
       if (threadIdx.x == 0) atomicExch(SA.err, 1u);
@@ -653,10 +662,10 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     const int g0 = S.fgstart[lc];
     if (g0 < 0) continue;
     const int i = t - S.fstart[lc];
-    const int nc = SA.mt.n[lc];
+    const int nc = S.mt_n[lc];
     double sx = 0, sy = 0, sz = 0;
     for (int k = 0; k < nc; ++k) {
-      const int he = SA.mt.he[lc][k];
+      const int he = S.mt_he[lc][k];
       const int hh = he >> 4, e = he & 15;
       if (!all_homes && S.hcell[hh] < 0) continue;  // (slab ranks: homes past the owned planes)
       const int s = S.sbase[hh][e] + i;
