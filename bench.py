@@ -314,8 +314,12 @@ def run_slab(args, rank, ws):
 
 
 def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True):
-    """Graph-replayed VV steps of one schedule, device-timed per phase with CUDA
-    events (L2 flushed before every step).  Returns the system and the timings."""
+    """Timed run: `steps` VV steps, each replayed as ONE CUDA graph (the
+    production path, LJSystem.graph_step), device-timed with CUDA events, L2
+    flushed before every step.  Breakdown run: up to 30 more steps replayed as
+    three graphs (pre | force | post) with events between the phases, for the
+    force-kernel time and the roofline.  Per-step counts stay on the device
+    (no host synchronisation inside either loop)."""
     if args.config == "cfg5":
         sysm = md.LJSystem.liquid_vapour(schedule=schedule, block=args.block, seed=42 + rank, skin=args.skin)
     else:
@@ -323,11 +327,16 @@ def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True):
     pre, force, post = sysm.graph_phases()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(args.warmup):
+        sysm.graph_step()
+    for _ in range(2):
         pre(); force(); post()
     torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
-    # per-step counts stay on the device (no host synchronisation inside the
-    # loop, so host launch latency is not timed); they are read at the end
+
+    def counts(hist, k):
+        hist[0, k].copy_(sysm.npairs[0])
+        hist[1, k].copy_(sysm.list_pairs_dev() if sysm.verlet else sysm.candidate_pairs_dev())
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
     hist = torch.zeros((2, steps), dtype=torch.int64, device="cuda")
     builds0 = int(sysm.graph_builds.item()) if sysm.verlet else 0
     barrier(ws)
@@ -337,30 +346,43 @@ def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True):
         clk.__enter__()
     try:
         for k in range(steps):
-            flush.zero_()  # L2 flush between timed steps (outside e[0]..e[3])
-            e = ev[k]
-            e[0].record(); pre(); e[1].record(); force(); e[2].record(); post(); e[3].record()
-            hist[0, k].copy_(sysm.npairs[0])
-            hist[1, k].copy_(sysm.list_pairs_dev() if sysm.verlet else sysm.candidate_pairs_dev())
+            flush.zero_()  # L2 flush between timed steps (outside e[0]..e[1])
+            ev[k][0].record()
+            sysm.graph_step()
+            ev[k][1].record()
+            counts(hist, k)
         torch.cuda.synchronize()
     finally:
         if clk:
             clk.__exit__(None, None, None)
     sysm.check_status()
+    builds = int(sysm.graph_builds.item()) - builds0 if sysm.verlet else None
     pairs, cands = hist[0].tolist(), hist[1].tolist()
     barrier(ws)
-    r = {"sys": sysm, "pairs": pairs, "cands": cands,
-         "step_ms": [e[0].elapsed_time(e[3]) for e in ev],
-         "force_ms": [e[1].elapsed_time(e[2]) for e in ev],
-         "pre_ms": [e[0].elapsed_time(e[1]) for e in ev],
-         "builds": int(sysm.graph_builds.item()) - builds0 if sysm.verlet else None,
+    # breakdown run
+    nb = min(steps, 30)
+    evb = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nb)]
+    histb = torch.zeros((2, nb), dtype=torch.int64, device="cuda")
+    for k in range(nb):
+        flush.zero_()
+        e = evb[k]
+        e[0].record(); pre(); e[1].record(); force(); e[2].record(); post(); e[3].record()
+        counts(histb, k)
+    torch.cuda.synchronize()
+    sysm.check_status()
+    pairs_b, cands_b = histb[0].tolist(), histb[1].tolist()
+    r = {"sys": sysm, "pairs": pairs, "cands": cands, "builds": builds,
+         "step_ms": [e[0].elapsed_time(e[1]) for e in ev],
+         "phase_step_ms": [e[0].elapsed_time(e[3]) for e in evb],
+         "force_ms": [e[1].elapsed_time(e[2]) for e in evb],
+         "pre_ms": [e[0].elapsed_time(e[1]) for e in evb],
          "clocks": clk.summary() if clk else None}
     r["tot_s"] = max_over_ranks(sum(r["step_ms"]) * 1e-3, ws)
     r["value"] = sum_over_ranks(float(sum(pairs)), ws) / r["tot_s"]
     # roofline of the dominant kernel: algorithmic FLOPs 8 C + 20 P,
     # C = candidates distance-tested (link-cell half shell, or Verlet list entries)
-    r["achieved"] = sum(8 * c + 20 * p for c, p in zip(cands, pairs)) / (sum(r["force_ms"]) * 1e-3) / 1e12
-    r["achieved_pairs"] = 20 * sum(pairs) / (sum(r["force_ms"]) * 1e-3) / 1e12
+    r["achieved"] = sum(8 * c + 20 * p for c, p in zip(cands_b, pairs_b)) / (sum(r["force_ms"]) * 1e-3) / 1e12
+    r["achieved_pairs"] = 20 * sum(pairs_b) / (sum(r["force_ms"]) * 1e-3) / 1e12
     return r
 
 
@@ -402,10 +424,13 @@ def run_ours(args):
            "l2": "flushed (256 MB memset) between timed steps",
            "steps_per_s": args.steps / tot_s, "pairs_per_step": statistics.mean(m["pairs"]),
            "candidates_per_step": statistics.mean(m["cands"]),
-           "force_ms_per_step": statistics.mean(m["force_ms"]),
-           "force_share": sum(m["force_ms"]) / sum(m["step_ms"]),
-           "pre_ms_per_step": statistics.mean(m["pre_ms"]), "pre_ms_median": statistics.median(m["pre_ms"]),
-           "pre_ms_max": max(m["pre_ms"]),
+           "phase_breakdown": {"steps": len(m["force_ms"]),
+                               "note": "separate run with the step split into 3 graphs (pre | force | post)",
+                               "ms_per_step": statistics.mean(m["phase_step_ms"]),
+                               "force_ms_per_step": statistics.mean(m["force_ms"]),
+                               "force_share": sum(m["force_ms"]) / sum(m["phase_step_ms"]),
+                               "pre_ms_per_step": statistics.mean(m["pre_ms"]),
+                               "pre_ms_median": statistics.median(m["pre_ms"]), "pre_ms_max": max(m["pre_ms"])},
            "parallelism": f"dp{ws}" if ws > 1 else "single"}
     if sysm.verlet:
         cfg.update({"skin": sysm.skin, "list_rebuilds_in_timed_steps": m["builds"],
