@@ -457,7 +457,8 @@ def run_ours(args):
                      "hbm_peak_gbs": peaks().get("hbm_gbs")},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": args.steps * sysm.launches_per_step(),
+        "gpu_launches": args.steps * sysm.launches_per_step()
+                        + (m["builds"] or 0) * getattr(sysm, "REBUILD_LAUNCHES", 0),
         "clocks": m["clocks"],
     }
     print(json.dumps(line), flush=True)

@@ -827,16 +827,26 @@ __global__ void k_gather_blocks(ShellArgs SA) {
       }
     }
   }
-  const unsigned have = __ballot_sync(CS_FULL, src >= 0);
+  // the <= 8 source offsets, then all loads issued before the fixed-order sums
+  int so[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) so[k] = __shfl_sync(CS_FULL, src, k);
   for (int i = lane; i < ((n + 31) & ~31); i += 32) {
+    double vx[8], vy[8], vz[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool ok = so[k] >= 0 && i < n;
+      const int64_t o = ok ? (int64_t)so[k] + i : 0;
+      vx[k] = ok ? __ldcs(SA.buf + o) : 0.0;
+      vy[k] = ok ? __ldcs(SA.buf + SA.bufstride + o) : 0.0;
+      vz[k] = ok ? __ldcs(SA.buf + 2 * SA.bufstride + o) : 0.0;
+    }
     double sx = 0, sy = 0, sz = 0;
-    for (unsigned m = have; m; m &= m - 1) {
-      const int o = __shfl_sync(CS_FULL, src, __ffs(m) - 1) + i;
-      if (i < n) {
-        sx += SA.buf[o];
-        sy += SA.buf[SA.bufstride + o];
-        sz += SA.buf[2 * SA.bufstride + o];
-      }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // same order as before: source lanes ascending
+      sx += vx[k];
+      sy += vy[k];
+      sz += vz[k];
     }
     if (i < n) {
       if (SA.overwrite) {
