@@ -38,9 +38,30 @@ WORKLOAD_CFG5 = ("cfg5: periodic 64x64x192 cells of edge 2.5 (160x160x480); FCC 
                  "elsewhere with no pair closer than 0.9; T* 0.85, rc 2.5, dt 0.005, fp64, 1 VV step")
 UNIT = "pair-interactions/s"
 NUC = 48  # cfg2
+# BASELINE configs run on one GPU: FCC cubes (cfg2 headline, cfg3, cfg4) and
+# the cfg5 liquid-vapour slab
+FCC_CONFIGS = {"cfg2": 48, "cfg3": 96, "cfg4": 192}
 WORKLOAD = ("cfg2: LJ fluid FCC 48^3 = 442368 particles, rho* 0.8442, T* 0.722, rc 2.5 (unshifted), "
             "dt 0.005, fp64, 1 VV step; link cells of edge >= rc (32^3) or, for the Verlet schedules, "
             ">= rc + skin (28^3)")
+
+
+def metric_of(config):
+    if config == "cfg5":
+        return METRIC_CFG5
+    if config == "cfg2":
+        return METRIC
+    n = 4 * FCC_CONFIGS[config] ** 3
+    return f"LJ link-cell pair interactions/s (fp64, {config} {n:,} particles)"
+
+
+def workload_of(config):
+    if config == "cfg5":
+        return WORKLOAD_CFG5
+    if config == "cfg2":
+        return WORKLOAD
+    k = FCC_CONFIGS[config]
+    return WORKLOAD.replace("cfg2: LJ fluid FCC 48^3 = 442368", f"{config}: LJ fluid FCC {k}^3 = {4 * k ** 3}")
 
 
 def traffic_bytes(schedule):
@@ -159,13 +180,15 @@ def cpu_setup(nthreads, config="cfg2"):
         vx, vy, vz = O.velocities(n, 0.85, 1.0, 42)
         return O.CpuMD(*(np.ascontiguousarray(xyz[:, k]) for k in range(3)), vx, vy, vz,
                        np.arange(n, dtype=np.int32), [64, 64, 192], list(L), nthreads=nthreads)
+    nuc = FCC_CONFIGS[config]
     rho = 0.8442
     a = (4 / rho) ** (1 / 3)
-    L = NUC * a
-    x, y, z = O.fcc_positions([NUC] * 3, [a] * 3, [L] * 3, 0.05, 42)
+    L = nuc * a
+    x, y, z = O.fcc_positions([nuc] * 3, [a] * 3, [L] * 3, 0.05, 42)
     n = len(x)
     vx, vy, vz = O.velocities(n, 0.722, 1.0, 42)
-    return O.CpuMD(x, y, z, vx, vy, vz, np.arange(n, dtype=np.int32), [32] * 3, [L] * 3, nthreads=nthreads)
+    nc = int(L // 2.5)
+    return O.CpuMD(x, y, z, vx, vy, vz, np.arange(n, dtype=np.int32), [nc] * 3, [L] * 3, nthreads=nthreads)
 
 
 def cpu_sample(nthreads, min_seconds=10.0, max_steps=200, config="cfg2"):
@@ -200,12 +223,12 @@ def run_reference(args):
     tot = sum(times)
     value = pairs / tot
     line = {
-        "impl": "reference", "metric": METRIC_CFG5 if args.config == "cfg5" else METRIC, "value": value,
+        "impl": "reference", "metric": metric_of(args.config), "value": value,
         "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded FCC + jitter, Gaussian velocities)",
-        "config": {"workload": WORKLOAD_CFG5 if args.config == "cfg5" else WORKLOAD,
+        "config": {"workload": workload_of(args.config),
                    "schedule": "loop-exchange colour order, 27 levels, OpenMP over tasks of a level",
                    "steps_per_s": args.steps / tot},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -323,7 +346,8 @@ def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True):
     if args.config == "cfg5":
         sysm = md.LJSystem.liquid_vapour(schedule=schedule, block=args.block, seed=42 + rank, skin=args.skin)
     else:
-        sysm = md.LJSystem.fcc(NUC, schedule=schedule, block=args.block, seed=42 + rank, skin=args.skin)
+        sysm = md.LJSystem.fcc(FCC_CONFIGS[args.config], schedule=schedule, block=args.block, seed=42 + rank,
+                               skin=args.skin)
     pre, force, post = sysm.graph_phases()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(args.warmup):
@@ -419,7 +443,7 @@ def run_ours(args):
                "sample": f"{nst} whole {args.config} VV steps in {el:.1f} s (oracle o_md_steps, loop-exchange colour order on OpenMP threads)"}
     n = sysm.n
     tot_s = m["tot_s"]
-    cfg = {"workload": WORKLOAD_CFG5 if args.config == "cfg5" else WORKLOAD, "particles_per_gpu": n, "schedule": f"{args.schedule} {sysm.block}",
+    cfg = {"workload": workload_of(args.config), "particles_per_gpu": n, "schedule": f"{args.schedule} {sysm.block}",
            "cells": list(sysm.box.cells),
            "l2": "flushed (256 MB memset) between timed steps",
            "steps_per_s": args.steps / tot_s, "pairs_per_step": statistics.mean(m["pairs"]),
@@ -439,13 +463,14 @@ def run_ours(args):
                               "particle moved > skin/2; every listed pair re-tested with r^2 < rc^2",
                     "link_cell_kernel": lc})
     line = {
-        "metric": METRIC_CFG5 if args.config == "cfg5" else METRIC, "value": m["value"], "unit": UNIT,
+        "metric": metric_of(args.config), "value": m["value"], "unit": UNIT,
         "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": ("synthetic (seeded liquid slab + rejection-sampled vapour, Gaussian velocities; BASELINE cfg5)"
                  if args.config == "cfg5" else
-                 "synthetic (seeded FCC 48^3 + 0.05 sigma jitter, Gaussian velocities; BASELINE cfg2)"),
+                 f"synthetic (seeded FCC {FCC_CONFIGS[args.config]}^3 + 0.05 sigma jitter, Gaussian velocities; "
+                 f"BASELINE {args.config})"),
         "config": cfg,
         "roofline": {"bound": "fp64", "achieved": m["achieved"], "peak": peak_fp64, "unit": "TFLOP/s",
                      "frac": m["achieved"] / peak_fp64, "traffic": traffic_bytes(args.schedule),
@@ -501,8 +526,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-link-cell", action="store_true", help="skip the link-cell comparison run")
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg5"],
-                    help="BASELINE workload: cfg2 (headline) or cfg5 (liquid-vapour load-imbalance stress)")
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="BASELINE workload on one GPU: cfg2 (headline), cfg3 (96^3 FCC), cfg4 (192^3 FCC), "
+                         "cfg5 (liquid-vapour load-imbalance stress)")
     ap.add_argument("--schedule", default="verlet",
                     choices=["shell", "buffered", "dataflow", "block", "loopex", "verlet", "verlet_shell",
                              "verlet_dataflow"])
