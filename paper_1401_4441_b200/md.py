@@ -541,6 +541,27 @@ class LJSystem:
     def candidate_pairs(self) -> int:
         return int(self.candidate_pairs_dev())
 
+    def rc_grid_candidates_dev(self):
+        """C of SURVEY 8(d)'s fixed convention: half-shell candidates on cells of
+        edge >= rc (floor(L / rc) per axis), counted from the current positions
+        on the device -- the same algorithmic work whatever the schedule."""
+        torch = _torch()
+        from .grid import canonical_half_stencil
+
+        b = self._buf[self.cur]
+        n = self.n
+        nc = [int(math.floor(L / self.params.rc)) for L in self.box.lengths]
+        idx = None
+        for k, key in enumerate(("x", "y", "z")):
+            L = self.box.lengths[k]
+            c = torch.floor(torch.remainder(b[key][:n], L) * (nc[k] / L)).long().clamp_(0, nc[k] - 1)
+            idx = c if idx is None else idx + c * int(math.prod(nc[:k]))
+        cnt = torch.bincount(idx, minlength=int(math.prod(nc))).view(nc[2], nc[1], nc[0])
+        c = (cnt * (cnt - 1) // 2).sum()
+        for ox, oy, oz in canonical_half_stencil(3).inter_offsets:
+            c = c + (cnt * torch.roll(cnt, shifts=(-oz, -oy, -ox), dims=(0, 1, 2))).sum()
+        return c
+
     def list_pairs_dev(self):
         """Verlet mode: pairs held in the current round tables, as a device
         scalar (each is distance-tested every step)."""
