@@ -61,9 +61,10 @@ struct ShellBase {
   int fstart[SH_MAXF + 1];           // footprint cell -> offset in the block buffer
   int fgstart[SH_MAXF];              // footprint cell -> global start (-1: none)
   int hcell[SH_MAXB];
+  int16_t mt_base[SH_MAXF][SH_MAXC];  // merge: slot base of each contributor (-1: home not owned)
   int overflow;
-  uint8_t mt_n[SH_MAXF];           // merge table in shared memory: lanes of one warp read
-  uint8_t mt_he[SH_MAXF][SH_MAXC];  //   different cells (divergent constant reads serialise)
+  uint8_t mt_n[SH_MAXF];           // merge-table counts in shared memory (lanes of one warp
+                                   //   read different cells: divergent constant reads serialise)
 };
 struct ShellSmem : ShellBase<SH_RCAP, SH_HCAP> {  // link-cell super-tasks
   double rows[SH_NW][SH_IB][3][32];  // per-lane i partials
@@ -404,6 +405,17 @@ __device__ __forceinline__ void shell_tables(const ShellArgs &SA, SM &S, const i
     }
   }
   __syncthreads();
+  for (int t = threadIdx.x; t < nfc * SH_MAXC; t += blockDim.x) {
+    const int lc = t / SH_MAXC, k = t - SH_MAXC * (t / SH_MAXC);
+    int base = -1;
+    if (k < SA.mt.n[lc]) {
+      const int he = SA.mt.he[lc][k];
+      const int hh = he >> 4, e = he & 15;
+      if (S.hcell[hh] >= 0) base = S.sbase[hh][e];
+    }
+    S.mt_base[lc][k] = (int16_t)base;
+  }
+  __syncthreads();
 }
 
 // bytes of the cached per-block tables: ShellBase from `sh` through `overflow`
@@ -451,11 +463,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   if (!cached) shell_tables<VERLET>(SA, S, o0);
   // merge table into shared memory (after the table copy, which may write
   // up to 15 padding bytes past `overflow`); read after later barriers
-  for (int k = threadIdx.x; k < SH_MAXF; k += blockDim.x) {
-    S.mt_n[k] = SA.mt.n[k];
-#pragma unroll
-    for (int c = 0; c < SH_MAXC; ++c) S.mt_he[k][c] = SA.mt.he[k][c];
-  }
+  for (int k = threadIdx.x; k < SH_MAXF; k += blockDim.x) S.mt_n[k] = SA.mt.n[k];
   if (S.overflow) {
     if constexpr (MODE != SH_COLOUR) {  // no in-place fallback: report to the host
       if (threadIdx.x == 0) atomicExch(SA.err, 1u);
@@ -647,7 +655,6 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   //         slots in the fixed merge-table order
   const int64_t boff = BUFFERED ? SA.boff[bid] : 0;
   const int nfoot = S.fstart[nfc];
-  const bool all_homes = __syncthreads_and(threadIdx.x >= nhome || S.hcell[threadIdx.x] >= 0);
   for (int t0 = wid * 32; t0 < nfoot; t0 += blockDim.x) {
     int lc = 0;  // footprint cell of t0 (lane 0), then step forward per lane
     if (lane == 0) {
@@ -665,10 +672,9 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     const int nc = S.mt_n[lc];
     double sx = 0, sy = 0, sz = 0;
     for (int k = 0; k < nc; ++k) {
-      const int he = S.mt_he[lc][k];
-      const int hh = he >> 4, e = he & 15;
-      if (!all_homes && S.hcell[hh] < 0) continue;  // (slab ranks: homes past the owned planes)
-      const int s = S.sbase[hh][e] + i;
+      const int base = S.mt_base[lc][k];
+      if (base < 0) continue;  // (slab ranks: homes past the owned planes)
+      const int s = base + i;
       sx += S.RF[0][s];
       sy += S.RF[1][s];
       sz += S.RF[2][s];
