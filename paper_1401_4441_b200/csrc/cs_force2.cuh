@@ -136,14 +136,16 @@ __device__ __forceinline__ bool verlet_pair(SM &S, const ForceArgs &A, int h, un
 
 // Newton-3 reaction of a hit into the (h, e) slot of j: no other lane writes
 // this slot in this round
+// (slot = S.sbase[h][entry] + index, looked up before the force math so its
+// latency is hidden; the three components are read before any is written)
 template <class SM>
-__device__ __forceinline__ void verlet_react(SM &S, int h, unsigned d, double fx, double fy,
-                                             double fz) {
+__device__ __forceinline__ void verlet_react(SM &S, int slot, double fx, double fy, double fz) {
   constexpr int stride = SM::RCAP + SM::HCAP;
-  double *dst = &S.RF[0][S.sbase[h][d >> 8] + (d & 255)];
-  dst[0] -= fx;
-  dst[stride] -= fy;
-  dst[2 * stride] -= fz;
+  double *dst = &S.RF[0][slot];
+  const double a = dst[0], b = dst[stride], c = dst[2 * stride];
+  dst[0] = a - fx;
+  dst[stride] = b - fy;
+  dst[2 * stride] = c - fz;
 }
 
 // Rounds are taken in pairs (the builder aligns switch rounds to even): the
@@ -192,6 +194,7 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, i
     const double x2 = __ldg(A.x + g), y2 = __ldg(A.y + g), z2 = __ldg(A.z + g);
     g = S.sstart[h][d3 >> 8] + (d3 & 255);
     const double x3 = __ldg(A.x + g), y3 = __ldg(A.y + g), z3 = __ldg(A.z + g);
+    const int slot0 = S.sbase[h][d0 >> 8] + (d0 & 255), slot1 = S.sbase[h][d1 >> 8] + (d1 & 255);
     double ux, uy, uz, vx, vy, vz;
     const bool h0 = verlet_pair<ENERGY, SHIFT>(S, A, h, d0, xi, yi, zi, x0, y0, z0, ux, uy, uz, pe);
     const bool h1 = verlet_pair<ENERGY, SHIFT>(S, A, h, d1, xi, yi, zi, x1, y1, z1, vx, vy, vz, pe);
@@ -199,9 +202,9 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, i
     fy_ += uy + vy;
     fz_ += uz + vz;
     hits += (unsigned)h0 + (unsigned)h1;
-    if (h0) verlet_react(S, h, d0, ux, uy, uz);
+    if (h0) verlet_react(S, slot0, ux, uy, uz);
     __syncwarp();
-    if (h1) verlet_react(S, h, d1, vx, vy, vz);
+    if (h1) verlet_react(S, slot1, vx, vy, vz);
     __syncwarp();
     d0 = d2;
     d1 = d3;
