@@ -703,7 +703,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
 }
 
 template <bool ENERGY, int MODE, bool VERLET>
-__global__ void __launch_bounds__(SH_NW * 32, 3) k_force_shell(ShellArgs SA, int colour) {
+__global__ void __launch_bounds__(SH_NW * 32, VERLET ? 2 : 3) k_force_shell(ShellArgs SA, int colour) {
   extern __shared__ __align__(16) unsigned char sh_raw[];
   if constexpr (MODE != SH_DATAFLOW) {
     shell_block<ENERGY, MODE, VERLET>(SA, sh_raw, colour, blockIdx.x);
