@@ -143,10 +143,32 @@ __device__ __forceinline__ unsigned long long vl_used<unsigned long long>(unsign
   return ((unsigned long long)used[1][j] << 32) | used[0][j];
 }
 
+// lowest free round of mask class `par` (0: any, 1: even, 2: odd) for a pair
+// whose j has rounds `u` taken: (round, segment) or -1
+template <class M>
+__device__ __forceinline__ int vl_pick(const M *fr, M u, M par, int &k) {
+  int r = -1;
+#pragma unroll
+  for (int kk = VB_SEG - 1; kk >= 0; --kk) {  // first segment with a free round wins
+    const M m = fr[kk] & ~u & par;
+    if (m) {
+      r = vl_ffs(m) - 1;
+      k = kk;
+    }
+  }
+  return r;
+}
+
+// Lockstep first-fit with two proposals per lane and iteration: pair A goes to
+// its lowest free round (either parity), pair B (another pending pair of the
+// chunk) to its lowest free round of the OTHER parity.  Even and odd proposals
+// never share a (j, round), so each parity resolves with its own match_any;
+// the lowest lane wins.
 template <class M>
 __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
                                          const int *seg_l, unsigned (*used)[VB_JCAP],
                                          const uint16_t *code, uint16_t (*tab)[32], int lane) {
+  const M EVEN = (M)0x5555555555555555ull, ODD = (M)0xAAAAAAAAAAAAAAAAull;
   bool ok = true;
   int cc = 0;
   unsigned cur = nch > 0 ? row[0] : 0u;
@@ -154,31 +176,44 @@ __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
   while (true) {
     while (cur == 0 && cc + 1 < nch) cur = row[++cc];
     if (!__any_sync(CS_FULL, cur != 0)) break;
-    const bool act = cur != 0;
-    const unsigned hi = cur & (~0u << rot);
-    const int b = act ? __ffs(hi ? hi : cur) - 1 : 0;
-    const int jl = cc * 32 + b;
-    int r = -1, k = 0;
-    if (act) {
-      const M u = vl_used<M>(used, jl);
-#pragma unroll
-      for (int kk = VB_SEG - 1; kk >= 0; --kk) {  // first segment with a free round wins
-        const M m = fr[kk] & ~u;
-        if (m) {
-          r = vl_ffs(m) - 1;
-          k = kk;
-        }
+    int bA = -1, bB = -1, rA = -1, rB = -1, kA = 0, kB = 0;
+    if (cur) {
+      const unsigned hi = cur & (~0u << rot);
+      bA = __ffs(hi ? hi : cur) - 1;
+      const unsigned rest = cur & ~(1u << bA);
+      if (rest) {
+        const unsigned hb = rest & (~0u << bA);
+        bB = __ffs(hb ? hb : rest) - 1;
       }
-      if (r < 0) {
+      const int jA = cc * 32 + bA;
+      rA = vl_pick<M>(fr, vl_used<M>(used, jA), ~(M)0, kA);
+      if (rA < 0) {  // no round left for a pending pair
         ok = false;
         cur = 0;
         cc = nch;
+        bB = -1;
+      } else if (bB >= 0) {
+        rB = vl_pick<M>(fr, vl_used<M>(used, cc * 32 + bB), (rA & 1) ? EVEN : ODD, kB);
       }
     }
-    const unsigned key = r >= 0 ? (unsigned)((jl << 6) | r) : (0x80000000u | lane);
-    const unsigned peers = __match_any_sync(CS_FULL, key);
+    const bool evA = rA >= 0 && !(rA & 1), pB = rB >= 0;
+    // even set: A if its round is even, else B; odd set: the other one
+    const int je = evA ? cc * 32 + bA : (pB ? cc * 32 + bB : 0), re = evA ? rA : (pB ? rB : -1);
+    const int jo = evA ? (pB ? cc * 32 + bB : 0) : (rA >= 0 ? cc * 32 + bA : 0);
+    const int ro = evA ? (pB ? rB : -1) : rA;
+    const unsigned keyE = re >= 0 ? (unsigned)((je << 6) | re) : (0x80000000u | lane);
+    const unsigned keyO = ro >= 0 ? (unsigned)((jo << 6) | ro) : (0x80000000u | lane);
+    const unsigned peersE = __match_any_sync(CS_FULL, keyE);
+    const unsigned peersO = __match_any_sync(CS_FULL, keyO);
     __syncwarp();
-    if (r >= 0 && __ffs(peers) - 1 == lane) {
+    const bool winE = re >= 0 && __ffs(peersE) - 1 == lane, winO = ro >= 0 && __ffs(peersO) - 1 == lane;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const bool win = t ? winO : winE;
+      if (!win) continue;
+      const int j = t ? jo : je, r = t ? ro : re;
+      const bool isA = (r == rA) && (j == cc * 32 + bA);
+      const int k = isA ? kA : kB, b = isA ? bA : bB;
       int tl = seg_l[0];
 #pragma unroll
       for (int kk = 0; kk < VB_SEG; ++kk)
@@ -187,8 +222,8 @@ __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
           tl = seg_l[kk];
         }
       cur &= ~(1u << b);
-      tab[r][tl] = code[jl];
-      atomicOr(&used[r >> 5][jl], 1u << (r & 31));  // native 32-bit shared atomic
+      tab[r][tl] = code[j];
+      atomicOr(&used[r >> 5][j], 1u << (r & 31));  // native 32-bit shared atomic
     }
     __syncwarp();
   }
