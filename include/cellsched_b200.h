@@ -141,6 +141,21 @@ int cs_payload_generic(int64_t ntasks, int dim, const int8_t *kind, const int32_
                        const int64_t *rptr, const int32_t *rres, const int64_t *q,
                        const int32_t *level, int64_t depth, int64_t nres, int64_t *val, void *ws,
                        size_t ws_bytes, void *stream);
+/* Device dependency-driven runtime: run the generic payload
+ * tasks (arguments as cs_payload_generic) in dependency order with a ready
+ * queue and indegree counters -- no level barriers.  Edges sorted by
+ * predecessor: successors of t are succ[sptr[t] .. sptr[t+1]), ev = the
+ * successor of every edge (nedges).  race_check != 0 counts write conflicts
+ * between concurrently running tasks into conflicts_dev[0] (executor
+ * exclusion contract).  CS_ECYCLE if a task is never released. */
+size_t cs_dag_ws_bytes(int64_t ntasks, int64_t nres);
+int cs_dag_execute(int64_t ntasks, int dim, const int8_t *kind, const int32_t *home,
+                   const int32_t *nbr, const int32_t *w0, const int32_t *w1, const int8_t *off,
+                   const int64_t *rptr, const int32_t *rres, const int64_t *q, int64_t nedges,
+                   const int64_t *sptr, const int64_t *succ, const int64_t *ev, int64_t nres,
+                   int64_t *val, int race_check, unsigned long long *conflicts_dev, void *ws,
+                   size_t ws_bytes, void *stream);
+
 /* The colour-pass schedules of the LJ kernel, run on the integer payload:
  * sched CS_SCHED_LOOPEX (27 passes) or CS_SCHED_BLOCK (8 block passes).
  * race_check != 0 records writers per pass and fails with CS_ECONFLICT. */

@@ -451,3 +451,152 @@ extern "C" size_t cs_payload_generic_ws_bytes(int64_t ntasks, int64_t depth) {
   return 2 * cs_ws_slice(sizeof(int32_t) * (ntasks + 1)) + 2 * cs_ws_slice(sizeof(int32_t) * (depth + 1)) +
          cs_scan_ws_bytes(depth) + 512;
 }
+
+// ------------------------------- device dependency-driven runtime --
+// Executes any task graph (apply_tasks semantics, payload.py:84-119) in
+// dependency order instead of level by level: a persistent grid pops tickets
+// from a ready queue, waits for the ticket's task, runs it, and releases its
+// successors (indegree counters; the last predecessor pushes).  Accumulators
+// are integers, so every valid order gives the reference's values.  With
+// race_check, every task marks the accumulators it writes for its duration;
+// finding a mark of another task counts a conflict -- the exclusion half of
+// executor.verify_execution (executor.py:357-377) checked on the device.
+struct DagArgs {
+  GTask T;
+  const int64_t *q;
+  int dim;
+  int64_t *val;
+  int32_t *indeg;
+  const int64_t *sptr;  // successors of t: succ[sptr[t] .. sptr[t+1])
+  const int64_t *succ;
+  int32_t *queue;
+  unsigned *head, *tail;
+  unsigned *mark;
+  unsigned long long *conflicts;
+  unsigned *err;
+  int64_t ntasks;
+  int race;
+};
+
+__global__ void k_dag_indeg(int64_t ne, const int64_t *ev, int32_t *indeg) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&indeg[ev[i]], 1);
+}
+
+__global__ void k_dag_roots(int64_t nt, const int32_t *indeg, int32_t *queue, unsigned *tail) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt;
+       t += (int64_t)gridDim.x * blockDim.x)
+    if (indeg[t] == 0) queue[atomicAdd(tail, 1u)] = (int32_t)t;
+}
+
+__device__ __forceinline__ void dag_claim(const DagArgs &D, int32_t w, int32_t t) {
+  const unsigned old = atomicExch(&D.mark[w], (unsigned)t + 1u);
+  if (old != 0u) atomicAdd(D.conflicts, 1ull);
+}
+
+__global__ void k_dag_run(DagArgs D) {
+  for (;;) {
+    const unsigned idx = atomicAdd(D.head, 1u);
+    if (idx >= (unsigned)D.ntasks) break;
+    int32_t t;
+    long long spins = 0;
+    while ((t = ((volatile int32_t *)D.queue)[idx]) < 0) {
+      if (++spins > (1ll << 26)) {  // never for a DAG: report instead of hanging
+        atomicOr(D.err, 1u);
+        return;
+      }
+      __nanosleep(64);
+    }
+    __threadfence();
+    const int k = D.T.kind[t];
+    const int32_t w0 = D.T.w0[t], w1 = D.T.w1[t];
+    if (D.race) {
+      dag_claim(D, w0, t);
+      if (k == 1 && w1 != w0) dag_claim(D, w1, t);
+    }
+    if (k == 0) {
+      D.val[w0] = __ldcg(D.val + w0) + pay_intra(D.q[D.T.home[t]]);
+    } else if (k == 1) {
+      const int8_t *o = D.T.off + 3 * (int64_t)t;
+      const int64_t g = pay_pair(D.q[D.T.home[t]], D.q[D.T.nbr[t]], o[0], o[1], o[2], D.dim);
+      D.val[w0] = __ldcg(D.val + w0) + g;
+      D.val[w1] = __ldcg(D.val + w1) - g;
+    } else {
+      int64_t s = 0;
+      for (int64_t r = D.T.rptr[t]; r < D.T.rptr[t + 1]; ++r) s += __ldcg(D.val + D.T.rres[r]);
+      D.val[w0] = __ldcg(D.val + w0) + s;
+    }
+    if (D.race) {
+      atomicExch(&D.mark[w0], 0u);
+      if (k == 1 && w1 != w0) atomicExch(&D.mark[w1], 0u);
+    }
+    __threadfence();
+    for (int64_t e = D.sptr[t]; e < D.sptr[t + 1]; ++e) {
+      const int64_t s = D.succ[e];
+      if (atomicSub(&D.indeg[s], 1) == 1) {
+        const unsigned pos = atomicAdd(D.tail, 1u);
+        atomicExch(&D.queue[pos], (int32_t)s);
+      }
+    }
+  }
+}
+
+extern "C" size_t cs_dag_ws_bytes(int64_t ntasks, int64_t nres) {
+  return 2 * cs_ws_slice(sizeof(int32_t) * (ntasks + 1)) + cs_ws_slice(sizeof(unsigned) * (nres + 1)) +
+         cs_ws_slice(64);
+}
+
+// eu/ev: edges sorted by eu (successor lists); sptr[ntasks+1] their offsets.
+extern "C" int cs_dag_execute(int64_t ntasks, int dim, const int8_t *kind, const int32_t *home,
+                              const int32_t *nbr, const int32_t *w0, const int32_t *w1,
+                              const int8_t *off, const int64_t *rptr, const int32_t *rres,
+                              const int64_t *q, int64_t nedges, const int64_t *sptr,
+                              const int64_t *succ, const int64_t *ev, int64_t nres, int64_t *val,
+                              int race_check, unsigned long long *conflicts_dev, void *ws,
+                              size_t ws_bytes, void *stream) {
+  cudaStream_t st = cs_stream(stream);
+  CS_CUDA(cudaMemsetAsync(val, 0, sizeof(int64_t) * nres, st));
+  if (ntasks == 0) return CS_OK;
+  cs_ws w(ws, ws_bytes);
+  CS_WS_TAKE(w, int32_t, indeg, ntasks + 1);
+  CS_WS_TAKE(w, int32_t, queue, ntasks + 1);
+  CS_WS_TAKE(w, unsigned, mark, nres + 1);
+  CS_WS_TAKE(w, unsigned, ctr, 16);
+  CS_CUDA(cudaMemsetAsync(indeg, 0, sizeof(int32_t) * (ntasks + 1), st));
+  CS_CUDA(cudaMemsetAsync(queue, 0xFF, sizeof(int32_t) * (ntasks + 1), st));  // -1: not pushed
+  CS_CUDA(cudaMemsetAsync(mark, 0, sizeof(unsigned) * (nres + 1), st));
+  CS_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 16, st));
+  if (conflicts_dev) CS_CUDA(cudaMemsetAsync(conflicts_dev, 0, sizeof(unsigned long long), st));
+  if (nedges > 0) k_dag_indeg<<<grid_for(nedges, 256), 256, 0, st>>>(nedges, ev, indeg);
+  DagArgs D;
+  D.T = GTask{kind, home, nbr, w0, w1, off, rptr, rres};
+  D.q = q;
+  D.dim = dim;
+  D.val = val;
+  D.indeg = indeg;
+  D.sptr = sptr;
+  D.succ = succ;
+  D.queue = queue;
+  D.head = ctr;
+  D.tail = ctr + 1;
+  D.err = ctr + 2;
+  D.mark = mark;
+  D.conflicts = conflicts_dev ? conflicts_dev : (unsigned long long *)(ctr + 4);
+  D.ntasks = ntasks;
+  D.race = race_check ? 1 : 0;
+  k_dag_roots<<<grid_for(ntasks, 256), 256, 0, st>>>(ntasks, indeg, queue, ctr + 1);
+  int dev = 0, nsm = 0;
+  CS_CUDA(cudaGetDevice(&dev));
+  CS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t threads = (int64_t)nsm * 4 * 128;
+  k_dag_run<<<(unsigned)((threads < ntasks ? threads : ntasks) + 127) / 128, 128, 0, st>>>(D);
+  unsigned err = 0;
+  CS_CUDA(cudaMemcpyAsync(&err, ctr + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CS_CUDA(cudaStreamSynchronize(st));
+  if (err) {
+    cs_set_error("dag_execute: a task was never released (cycle in the edge list?)");
+    return CS_ECYCLE;
+  }
+  return cs_check_launch("dag_execute");
+}

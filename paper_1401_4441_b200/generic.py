@@ -94,16 +94,12 @@ def longest_path_device(ntasks, edges, return_levels=False):
     return depth.value
 
 
-def apply_tasks_generic(tasks, grid, seed):
-    """apply_tasks (payload.py:84-119) for any accumulator / buffered stream,
-    executed level by level on the device."""
-    torch = _torch()
+def _payload_arrays(tasks, grid):
+    """Per-task payload descriptors of apply_tasks (payload.py:84-119) with
+    resources interned to dense accumulator ids."""
     from .grid import neighbor
-    from .payload import _signed64, charges_device
     from .taskgen import INTER, INTRA, REDUCE, accumulator
 
-    _lib.require_cuda()
-    tasks = list(tasks)
     ids, tptr, at, ar, aw = _intern(tasks)
     nt = len(tasks)
     kind = np.zeros(nt, np.int8)
@@ -139,22 +135,86 @@ def apply_tasks_generic(tasks, grid, seed):
         else:
             raise ValueError(f"task {t.id} has non-payload kind {t.kind!r}")
         rptr.append(len(rres))
+    return ids, [kind, home, nbr, w0, w1, off.ravel(), np.asarray(rptr, np.int64), np.asarray(rres, np.int32)]
+
+
+
+
+def _dev(a, dtype):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda") if len(a) else torch.zeros(1, dtype=dtype, device="cuda")
+
+
+def _result(grid, ids, val):
+    from .taskgen import accumulator
+
+    vals = val.cpu().tolist()
+    return {c: (vals[ids[accumulator(c)]] if accumulator(c) in ids else 0) for c in grid.cells()}
+
+
+def apply_tasks_generic(tasks, grid, seed):
+    """apply_tasks (payload.py:84-119) for any accumulator / buffered stream,
+    executed level by level on the device."""
+    torch = _torch()
+    from .payload import _signed64, charges_device
+
+    _lib.require_cuda()
+    tasks = list(tasks)
+    ids, arrs = _payload_arrays(tasks, grid)
+    nt = len(tasks)
     from .depgraph import detect_dependencies
 
     graph = detect_dependencies(tasks)
     depth, levels = longest_path_device(nt, graph.edges, return_levels=True)
-    dev = "cuda"
-    T = lambda a, dt=None: torch.from_numpy(np.ascontiguousarray(a)).to(dev) if len(a) else torch.zeros(1, dtype=dt, device=dev)
+    dts = [torch.int8, torch.int32, torch.int32, torch.int32, torch.int32, torch.int8, torch.int64, torch.int32]
+    args = [_dev(a, dt) for a, dt in zip(arrs, dts)]
     q = charges_device(grid, _signed64(seed))
     nres = max(len(ids), 1)
-    val = torch.zeros(nres, dtype=torch.int64, device=dev)
-    lv = torch.tensor(levels, dtype=torch.int32, device=dev)
+    val = torch.zeros(nres, dtype=torch.int64, device="cuda")
+    lv = torch.tensor(levels, dtype=torch.int32, device="cuda")
     wsb = _lib.load().cs_payload_generic_ws_bytes(nt, depth)
-    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
-    args = [T(kind, torch.int8), T(home, torch.int32), T(nbr, torch.int32), T(w0, torch.int32),
-            T(w1, torch.int32), T(off.ravel(), torch.int8), T(np.asarray(rptr, np.int64), torch.int64),
-            T(np.asarray(rres, np.int32), torch.int32)]
+    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device="cuda")
     _lib.call("cs_payload_generic", nt, grid.dim, *(_lib.ptr(a) for a in args), _lib.ptr(q),
               _lib.ptr(lv), depth, nres, _lib.ptr(val), _lib.ptr(ws), wsb, _lib.stream_handle())
-    vals = val.cpu().tolist()
-    return {c: (vals[ids[accumulator(c)]] if accumulator(c) in ids else 0) for c in grid.cells()}
+    return _result(grid, ids, val)
+
+
+def execute_dag(tasks, grid, seed, race_check: bool = True, edges=None):
+    """run any task graph on the device in dependency order (ready
+    queue + indegree counters, no levels) with the apply_tasks payload.
+    Returns (accumulators by cell, write conflicts observed); with the
+    reference's dependency rule the conflicts are 0 and the accumulators equal
+    reference_oracle's -- executor.verify_execution's contract (executor.py:357-377)."""
+    torch = _torch()
+    from .payload import _signed64, charges_device
+
+    _lib.require_cuda()
+    tasks = list(tasks)
+    nt = len(tasks)
+    ids, arrs = _payload_arrays(tasks, grid)
+    if edges is None:
+        eu, ev = detect_edges_generic(tasks)
+    else:  # caller-supplied dependencies (tests: a wrong graph must show conflicts)
+        e = np.asarray(list(edges), np.int64).reshape(-1, 2)
+        eu, ev = e[:, 0], e[:, 1]
+    order = np.argsort(eu, kind="stable")
+    eu, ev = eu[order].astype(np.int64), ev[order].astype(np.int64)
+    sptr = np.zeros(nt + 1, np.int64)
+    np.cumsum(np.bincount(eu, minlength=nt), out=sptr[1:])
+    dts = [torch.int8, torch.int32, torch.int32, torch.int32, torch.int32, torch.int8, torch.int64, torch.int32]
+    args = [_dev(a, dt) for a, dt in zip(arrs, dts)]
+    q = charges_device(grid, _signed64(seed))
+    nres = max(len(ids), 1)
+    val = torch.zeros(nres, dtype=torch.int64, device="cuda")
+    d_sptr, d_succ, d_ev = _dev(sptr, torch.int64), _dev(ev, torch.int64), _dev(ev, torch.int64)
+    conflicts = torch.zeros(1, dtype=torch.int64, device="cuda")
+    wsb = _lib.load().cs_dag_ws_bytes(nt, nres)
+    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device="cuda")
+    st = _lib.load().cs_dag_execute(nt, grid.dim, *(_lib.ptr(a) for a in args), _lib.ptr(q), len(ev),
+                                    _lib.ptr(d_sptr), _lib.ptr(d_succ), _lib.ptr(d_ev), nres,
+                                    _lib.ptr(val), 1 if race_check else 0, _lib.ptr(conflicts),
+                                    _lib.ptr(ws), wsb, _lib.stream_handle())
+    if st == _lib.CS_ECYCLE:
+        raise RuntimeError(_lib.load().cs_last_error().decode())
+    _lib.check(st, "cs_dag_execute")
+    return _result(grid, ids, val), int(conflicts.item())
