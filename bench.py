@@ -265,16 +265,20 @@ def run_slab(args, rank, ws):
     from paper_1401_4441_b200 import _lib, md, slab
 
     dev = torch.cuda.current_device()
-    if args.schedule not in ("shell", "buffered", "dataflow", "block", "loopex"):
-        args.schedule = "buffered"  # the slab engine runs the link-cell kernels
+    verlet = args.schedule in md.VERLET_SCHEDULES
+    if verlet:
+        args.schedule = "verlet"  # buffered block schedule on the rank-local grid
     nuc = (NUC * ws, NUC, NUC)
     box, nucs, a = md.fcc_box(nuc, 0.8442)
     n = 4 * nucs[0] * nucs[1] * nucs[2]
     g = md.LJSystem(box, n, schedule="loopex")  # global initial state (same on every rank)
     g.seed_fcc(nucs, a, 0.722, 0.05, 42)
     ini = {k: v[:n] for k, v in g.initial.items()}
+    if verlet:  # cells of edge >= rc + skin (y, z multiples of 4 for the block colouring)
+        c = md.LJBox.for_cutoff(box.lengths, 2.5 + args.skin).cells
+        box = md.LJBox(box.lengths, (c[0] - c[0] % (2 * ws),) + tuple(v - v % 4 for v in c[1:]))
     lay = slab.SlabLayout(box.cells[0], ws, rank)
-    eng = slab.CudaSlabEngine(box, lay, md.LJParams(), schedule=args.schedule)
+    eng = slab.CudaSlabEngine(box, lay, md.LJParams(), schedule=args.schedule, skin=args.skin)
     eng.load_global(ini["x"], ini["y"], ini["z"], ini["vx"], ini["vy"], ini["vz"], ini["id"])
     del g
     torch.cuda.empty_cache()
@@ -285,24 +289,24 @@ def run_slab(args, rank, ws):
         st.step()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    pairs = 0
+    p0 = st.pairs_total()
     with ClockSampler(dev) as clk:
         for k in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             barrier(ws)
             ev[k][0].record()
-            out = st.step(energy=False)
+            st.step(energy=False, reduce=False)  # pair counts stay on the device
             ev[k][1].record()
             torch.cuda.synchronize()
-            pairs += out["pairs"]  # already summed over ranks
+    pairs = st.pairs_total() - p0  # summed over ranks
     tot_s = max_over_ranks(sum(e0.elapsed_time(e1) for e0, e1 in ev) * 1e-3, ws)
     # e2e: host buffers in, K steps with per-step energy readback, host buffers out
     hx = {k: v.cpu().pin_memory() for k, v in ini.items()}
     barrier(ws)
     t0 = time.perf_counter()
     dx = {k: v.to("cuda", non_blocking=True) for k, v in hx.items()}
-    eng2 = slab.CudaSlabEngine(box, lay, md.LJParams(), schedule=args.schedule)
+    eng2 = slab.CudaSlabEngine(box, lay, md.LJParams(), schedule=args.schedule, skin=args.skin)
     eng2.load_global(dx["x"], dx["y"], dx["z"], dx["vx"], dx["vy"], dx["vz"], dx["id"])
     st2 = slab.SlabStep(eng2, slab.NeighbourExchanger(lay))
     st2.start(energy=True)
@@ -321,8 +325,10 @@ def run_slab(args, rank, ws):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded FCC + 0.05 sigma jitter, Gaussian velocities)",
         "config": {"workload": f"cfg2 per GPU, x-slab weak scaling: FCC {nuc[0]}x48x48 = {n} particles, "
-                               f"{box.cells[0]}x32x32 cells, {lay.owned} planes per rank",
-                   "schedule": f"{args.schedule} (2, 2, 2) on the rank-local grid",
+                               f"{box.cells[0]}x{box.cells[1]}x{box.cells[2]} cells, {lay.owned} planes per rank",
+                   "schedule": f"{args.schedule} (2, 2, 2) on the rank-local grid"
+                               + (f", skin {args.skin}, list rebuilds {st.rebuilds} (all ranks together, "
+                                  "migration only at rebuilds)" if verlet else ""),
                    "l2": "flushed (256 MB memset) between timed steps",
                    "parallelism": f"x-slab{ws}: ghost plane + reverse forces + migration over NCCL send/recv",
                    "steps_per_s": args.steps / tot_s},

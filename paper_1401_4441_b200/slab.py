@@ -106,6 +106,21 @@ class NeighbourExchanger:
                    if op[0].numel() > 0])
         return from_left, from_right
 
+    def exchange_fixed(self, to_left, to_right, n_from_left, n_from_right):
+        """Same as exchange() when both sides already know the sizes (a Verlet
+        slab between rebuilds): payloads only, no size round trip."""
+        torch = _torch()
+        L = self.layout
+        if L.world == 1:
+            return to_right, to_left
+        dev = to_left.device
+        from_right = torch.empty(n_from_right, dtype=to_left.dtype, device=dev)
+        from_left = torch.empty(n_from_left, dtype=to_left.dtype, device=dev)
+        self._run([op for op in ((to_left, L.left, 1, True), (to_right, L.right, 2, True),
+                                 (from_right, L.right, 1, False), (from_left, L.left, 2, False))
+                   if op[0].numel() > 0])
+        return from_left, from_right
+
     def _run(self, ops):
         import torch.distributed as dist
 
@@ -125,6 +140,19 @@ class NeighbourExchanger:
             for w in works:
                 w.wait()
 
+    def allreduce_max_int(self, value: int) -> int:
+        """Global OR / max of a small integer (the Verlet rebuild decision)."""
+        torch = _torch()
+        if self.layout.world == 1:
+            return int(value)
+        import torch.distributed as dist
+
+        t = torch.tensor([int(value)], dtype=torch.int64)
+        if dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
     def allreduce_sum(self, values):
         torch = _torch()
         t = torch.tensor(values, dtype=torch.float64)
@@ -143,39 +171,76 @@ class SlabStep:
 
     def __init__(self, engine, exchanger: NeighbourExchanger):
         self.e, self.x = engine, exchanger
+        # Verlet engines migrate and rebin only at list rebuilds, which every
+        # rank takes in the same step (global OR of the displacement flags);
+        # in between, the ghost plane keeps its particles and order
+        self.verlet = bool(getattr(engine, "verlet", False))
+        self.rebuilds = 0
 
     def migrate(self):
         stay, to_left, to_right = self.e.split()
         from_left, from_right = self.x.exchange(to_left, to_right)
         self.e.assemble(stay, from_left, from_right)
 
-    def forces(self, energy: bool):
+    def forces(self, energy: bool, rebuild: bool = True):
         L = self.x.layout
-        counts, xyz = self.e.pack_first_plane(xshift=self.e.box_length_x if L.rank == 0 else 0.0)
+        fixed = self.verlet and not rebuild  # same ghost particles, same order, same sizes
+        counts, xyz = self.e.pack_first_plane(xshift=self.e.box_length_x if L.rank == 0 else 0.0,
+                                              cached=fixed)
         # positions of my first plane go left; the right rank's first plane is my ghost
-        g_counts_l, g_counts_r = self.x.exchange(counts, counts[:0])
-        g_xyz_l, g_xyz_r = self.x.exchange(xyz, xyz[:0])
-        self.e.set_ghosts(g_counts_r, g_xyz_r)
-        pe, npairs = self.e.forces(energy)
+        if fixed:
+            _, g_xyz_r = self.x.exchange_fixed(xyz, xyz[:0], 0, 3 * self.e.n_ghost)
+            self.e.set_ghosts(self._g_counts, g_xyz_r)
+        else:
+            g_counts_l, g_counts_r = self.x.exchange(counts, counts[:0])
+            g_xyz_l, g_xyz_r = self.x.exchange(xyz, xyz[:0])
+            self._g_counts = g_counts_r
+            self._n_first = xyz.numel() // 3
+            self.e.set_ghosts(g_counts_r, g_xyz_r)
+        if self.verlet and rebuild:
+            self.e.build_list()
+        pe, npairs = self.e.forces(energy, sync=not fixed or energy)
         # reactions on my ghost plane go back to its owner (the right rank)
         fg = self.e.pack_ghost_forces()
-        f_from_left, _ = self.x.exchange(fg[:0], fg)
+        if fixed:
+            f_from_left, _ = self.x.exchange_fixed(fg[:0], fg, 3 * self._n_first, 0)
+        else:
+            f_from_left, _ = self.x.exchange(fg[:0], fg)
         self.e.add_first_plane_forces(f_from_left)
         return pe, npairs
 
-    def start(self, energy=True):
+    def _rebuild(self):
+        if self.verlet:
+            self.e.wrap()
         self.migrate()
         self.e.build_cells()
-        pe, npairs = self.forces(energy)
+        self.rebuilds += 1
+
+    def start(self, energy=True):
+        self._rebuild()
+        pe, npairs = self.forces(energy, rebuild=True)
         return self._energies(pe, npairs, energy)
 
-    def step(self, energy: bool = False):
+    def step(self, energy: bool = False, reduce: bool = True):
+        """One VV step.  reduce=False (non-energy steps) skips the global sums:
+        pair counts stay in the engine's device accumulator (pairs_total)."""
         self.e.kick_drift()
-        self.migrate()
-        self.e.build_cells()
-        pe, npairs = self.forces(energy)
+        rebuild = True
+        if self.verlet:
+            rebuild = self.x.allreduce_max_int(self.e.take_flag()) > 0
+        if rebuild:
+            self._rebuild()
+        pe, npairs = self.forces(energy, rebuild=rebuild)
         self.e.kick()
+        if not reduce and not energy:
+            return None
         return self._energies(pe, npairs, energy)
+
+    def pairs_total(self) -> int:
+        """Pairs accumulated on the device over all force evaluations, summed
+        over ranks (one synchronisation)."""
+        tot = self.x.allreduce_sum([float(self.e.pairs_acc.item())])
+        return int(tot[0])
 
     def _energies(self, pe, npairs, energy):
         ke = self.e.kinetic() if energy else 0.0
@@ -187,13 +252,17 @@ class CudaSlabEngine:
     """Rank-local state and C ABI kernels for one x-slab on one GPU."""
 
     def __init__(self, box, layout: SlabLayout, params, schedule="buffered", block=(2, 2, 2),
-                 capacity: int | None = None, dt: float = 0.005, device=None):
+                 capacity: int | None = None, dt: float = 0.005, device=None, skin: float = 0.3):
         torch = _torch()
         _lib.require_cuda()
-        from .md import SCHEDULES
+        from .md import SCHEDULES, VERLET_SCHEDULES
 
         self.box, self.layout, self.params, self.dt = box, layout, params, dt
         self.schedule = schedule
+        self.verlet = schedule in VERLET_SCHEDULES
+        self.skin = float(skin) if self.verlet else 0.0
+        if self.verlet and min(box.cell_edge) < (params.rc + self.skin) * (1 - 1e-12):
+            raise ValueError("Verlet slabs need cells of edge >= rc + skin")
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         nx, ny, nz = box.cells
         owned = layout.owned
@@ -244,8 +313,13 @@ class CudaSlabEngine:
         self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=d)
         self.scal = torch.zeros(8, dtype=f64, device=d)
         self.npairs = torch.zeros(1, dtype=torch.int64, device=d)
+        self.pairs_acc = torch.zeros(1, dtype=torch.int64, device=d)
         self.status = torch.zeros(1, dtype=torch.int32, device=d)
         self.counts = torch.zeros(self.plane_cells, dtype=torch.int32, device=d)
+        if self.verlet:
+            self.vlist = torch.zeros(int(L.cs_verlet_list_bytes(C.byref(self.cbox))), dtype=torch.uint8, device=d)
+            self.xref = [torch.zeros(cap, dtype=f64, device=d) for _ in range(3)]
+            self.vflag = torch.zeros(1, dtype=torch.int32, device=d)
 
     def _s(self):
         return _lib.stream_handle()
@@ -276,10 +350,35 @@ class CudaSlabEngine:
     def kick_drift(self):
         a = self.A
         hdtm = 0.5 * self.dt / self.params.mass
+        if self.verlet:  # no wrap between rebuilds; flag particles past skin/2
+            _lib.call("cs_vv_kick_drift_track", self.n_owned, hdtm, self.dt, _lib.ptr(a["fx"]),
+                      _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), _lib.ptr(a["vx"]), _lib.ptr(a["vy"]),
+                      _lib.ptr(a["vz"]), _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]),
+                      *(_lib.ptr(t) for t in self.xref), 0.5 * self.skin, _lib.ptr(self.vflag), self._s())
+            return
         _lib.call("cs_vv_kick_drift", self.n_owned, hdtm, self.dt, C.byref(self.cbox),
                   _lib.ptr(a["fx"]), _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), _lib.ptr(a["vx"]),
                   _lib.ptr(a["vy"]), _lib.ptr(a["vz"]), _lib.ptr(a["x"]), _lib.ptr(a["y"]),
                   _lib.ptr(a["z"]), self._s())
+
+    def take_flag(self) -> int:
+        """Verlet mode: this rank's displacement flag (cleared)."""
+        v = int(self.vflag.item())
+        self.vflag.zero_()
+        return v
+
+    def wrap(self):
+        a = self.A
+        _lib.call("cs_wrap_positions", self.n_owned, C.byref(self.cbox), _lib.ptr(a["x"]), _lib.ptr(a["y"]),
+                  _lib.ptr(a["z"]), self._s())
+
+    def build_list(self):
+        """Round tables over the local grid (owned planes + the ghost plane)."""
+        a = self.A
+        _lib.call("cs_verlet_build", C.byref(self.cbox), C.byref(self.clj), self.skin,
+                  _lib.ptr(self.cell_start), _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]),
+                  _lib.ptr(self.vlist), self.vlist.numel(), *(_lib.ptr(t) for t in self.xref),
+                  self.n_owned, _lib.ptr(self.status), self._s())
 
     def kick(self):
         a = self.A
@@ -326,12 +425,16 @@ class CudaSlabEngine:
                   _lib.ptr(self.ws), self.wsb, self._s())
         self.A, self.B = self.B, self.A
 
-    def pack_first_plane(self, xshift):
+    def pack_first_plane(self, xshift, cached: bool = False):
         torch = _torch()
-        rng = (C.c_int64 * 2)()
-        _lib.call("cs_plane_counts", C.byref(self.cbox), 0, _lib.ptr(self.cell_start),
-                  _lib.ptr(self.counts), rng, self._s())
-        m = rng[1] - rng[0]
+        if cached:  # Verlet between rebuilds: same cells, same particle range
+            m = self._first_m
+        else:
+            rng = (C.c_int64 * 2)()
+            _lib.call("cs_plane_counts", C.byref(self.cbox), 0, _lib.ptr(self.cell_start),
+                      _lib.ptr(self.counts), rng, self._s())
+            m = rng[1] - rng[0]
+            self._first_m = m
         out = torch.empty(3 * m, dtype=torch.float64, device=self.device)
         a = self.A
         _lib.call("cs_pack_plane", C.byref(self.cbox), 0, _lib.ptr(self.cell_start), _lib.ptr(a["x"]),
@@ -351,15 +454,30 @@ class CudaSlabEngine:
                   _lib.ptr(a["fz"]), _lib.ptr(self.ws), self.wsb, self._s())
         self.n_ghost = m
 
-    def forces(self, energy):
+    def forces(self, energy, sync: bool = True):
+        """Local forces.  sync=False (Verlet, between rebuilds, no energy): no
+        host reads; pairs go to the device accumulator only."""
         a = self.A
         self.scal[0:1].zero_()
         self.npairs.zero_()
+        if self.verlet:
+            _lib.call("cs_lj_forces_verlet", C.byref(self.cbox), C.byref(self.clj), self.sched,
+                      self.n_owned + self.n_ghost, _lib.ptr(self.cell_start), _lib.ptr(self.vlist),
+                      _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]), _lib.ptr(a["fx"]),
+                      _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), _lib.ptr(self.scal) if energy else None,
+                      _lib.ptr(self.npairs), _lib.ptr(self.status), _lib.ptr(self.ws), self.wsb, self._s())
+            self.pairs_acc += self.npairs
+            if not sync:
+                return 0.0, 0
+            if int(self.status.item()):
+                raise _lib.CellschedError("Verlet slab: kernel capacity flag %d" % int(self.status.item()))
+            return float(self.scal[0].item()) if energy else 0.0, int(self.npairs.item())
         _lib.call("cs_lj_forces", C.byref(self.cbox), C.byref(self.clj), self.sched,
                   self.n_owned + self.n_ghost, _lib.ptr(self.cell_start), _lib.ptr(a["x"]),
                   _lib.ptr(a["y"]), _lib.ptr(a["z"]), _lib.ptr(a["fx"]), _lib.ptr(a["fy"]),
                   _lib.ptr(a["fz"]), _lib.ptr(self.scal) if energy else None, _lib.ptr(self.npairs),
                   _lib.ptr(self.status), _lib.ptr(self.ws), self.wsb, self._s())
+        self.pairs_acc += self.npairs
         if int(self.status.item()):
             raise _lib.CellschedError("force kernel capacity overflow (use schedule='shell')")
         return float(self.scal[0].item()) if energy else 0.0, int(self.npairs.item())

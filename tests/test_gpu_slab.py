@@ -32,6 +32,9 @@ class ThreadRingExchanger(slab.NeighbourExchanger):
         hub["bar"].wait()
         return from_left, from_right
 
+    def exchange_fixed(self, to_left, to_right, n_from_left, n_from_right):
+        return self.exchange(to_left, to_right)
+
     def allreduce_sum(self, values):
         L, hub = self.layout, self.hub
         hub["box"][(L.rank, "sum")] = list(values)
@@ -101,3 +104,74 @@ def test_slab_one_rank_ring(oracle, cuda, schedule):
 @pytest.mark.parametrize("world,schedule", [(2, "buffered"), (2, "loopex"), (3, "shell")])
 def test_slab_virtual_ranks(oracle, cuda, world, schedule):
     _run(world, 12, 4, schedule, oracle, cuda)
+
+
+def _run_verlet(world, nuc, steps, skin, oracle, cuda):
+    """Verlet slabs: cells of edge >= rc + skin, list rebuilds (with migration)
+    taken by every rank together, ghost plane refreshed in place between them."""
+    torch = cuda
+    box0, nucs, a = md.fcc_box(nuc, RHO)
+    cells = md.LJBox.for_cutoff(box0.lengths, 2.5 + skin).cells
+    box = md.LJBox(box0.lengths, (cells[0],) + tuple(c - c % 4 for c in cells[1:]))
+    ref_sys = md.LJSystem.fcc(nuc, schedule="verlet", skin=skin)  # the seeded initial state
+    ini = ref_sys.initial
+    n = ref_sys.n
+    hub = {"box": {}, "bar": threading.Barrier(world)}
+    results, errors = {}, []
+
+    class Ring(ThreadRingExchanger):
+        def allreduce_max_int(self, value):
+            L, hub = self.layout, self.hub
+            hub["box"][(L.rank, "max")] = int(value)
+            hub["bar"].wait()
+            m = max(hub["box"][(r, "max")] for r in range(L.world))
+            hub["bar"].wait()
+            return m
+
+    def rank_main(r):
+        try:
+            lay = slab.SlabLayout(box.cells[0], world, r)
+            eng = slab.CudaSlabEngine(box, lay, md.LJParams(), schedule="verlet", skin=skin)
+            eng.load_global(*(ini[k][:n] for k in ("x", "y", "z", "vx", "vy", "vz", "id")))
+            ex = Ring(lay, hub) if world > 1 else slab.NeighbourExchanger(lay)
+            st = slab.SlabStep(eng, ex)
+            out = [st.start(energy=True)]
+            f0 = eng.owned_arrays()
+            for _ in range(steps):
+                out.append(st.step(energy=True))
+            torch.cuda.synchronize()
+            results[r] = (out, f0, st.rebuilds)
+        except Exception as exc:
+            errors.append(exc)
+            hub["bar"].abort()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errors:
+        raise errors[0]
+    hx = {k: ini[k][:n].cpu().numpy() for k in ini}
+    ref = oracle.md_run(hx["x"], hx["y"], hx["z"], hx["vx"], hx["vy"], hx["vz"], hx["id"],
+                        list(box.cells), list(box.lengths), steps)
+    ref0 = oracle.md_run(hx["x"], hx["y"], hx["z"], hx["vx"], hx["vy"], hx["vz"], hx["id"],
+                         list(box.cells), list(box.lengths), 0)
+    ids = np.concatenate([results[r][1]["id"] for r in range(world)])
+    f = np.concatenate([results[r][1]["f"] for r in range(world)])
+    assert sorted(ids.tolist()) == list(range(n))
+    fref = np.empty((n, 3))
+    fref[ref0["id"]] = ref0["f"]
+    frms = np.sqrt((fref ** 2).sum(1).mean())
+    err = np.linalg.norm(f - fref[ids], axis=1) / np.maximum(np.linalg.norm(fref[ids], axis=1), frms)
+    assert err.max() < 1e-10, err.max()
+    e = np.array([o["pe"] + o["ke"] for o in results[0][0]])
+    eref = ref["pe"] + ref["ke"]
+    assert np.abs(e - eref).max() / abs(eref[0]) < 1e-12
+    assert results[0][0][-1]["n"] == n
+    assert results[0][2] >= 2  # the initial build + at least one rebuild with migration
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_slab_verlet(oracle, cuda, world):
+    _run_verlet(world, 14, 10, 0.12, oracle, cuda)

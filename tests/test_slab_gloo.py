@@ -94,7 +94,7 @@ class CpuSlabEngine:
         self.x, self.v, self.id, self.c = self.x[o], self.v[o], self.id[o], c[o]
         self.f = np.zeros_like(self.x)
 
-    def pack_first_plane(self, xshift):
+    def pack_first_plane(self, xshift, cached=False):
         ny, nz = self.cells[1], self.cells[2]
         cx = self.c % self.nl[0]
         m = cx == 0
@@ -109,8 +109,9 @@ class CpuSlabEngine:
     def set_ghosts(self, counts, xyz):
         self.gx = xyz.numpy().reshape(3, -1).T.copy()
         self.gcount = counts.numpy().astype(int)
+        self.n_ghost = len(self.gx)
 
-    def forces(self, energy):
+    def forces(self, energy, sync=True):
         O = self.O
         ny, nz = self.cells[1], self.cells[2]
         gcell = np.repeat(np.arange(ny * nz), self.gcount)
@@ -141,7 +142,40 @@ class CpuSlabEngine:
         return 0.5 * float((self.v ** 2).sum())
 
 
-def _worker(rank, world, port, q):
+class CpuVerletSlabEngine(CpuSlabEngine):
+    """The Verlet-slab protocol on CPU: cells of edge >= rc + skin, no wrap and
+    no migration between list rebuilds (forces from the cell list of the last
+    rebuild stay exact, as for the device round tables)."""
+
+    verlet = True
+
+    def __init__(self, O, layout, cells, L, skin, dt=0.005):
+        super().__init__(O, layout, cells, L, dt)
+        self.skin = skin
+        self.flag = 0
+
+    def kick_drift(self):
+        self.v = self.v + 0.5 * self.dt * self.f
+        self.x = self.x + self.dt * self.v
+        d = ((self.x - self.x0) ** 2).sum(1)
+        self.flag = int((d > (0.5 * self.skin) ** 2).any())
+
+    def take_flag(self):
+        f, self.flag = self.flag, 0
+        return f
+
+    def wrap(self):
+        self.x = np.mod(self.x, np.asarray(self.L))
+
+    def build_cells(self):
+        super().build_cells()
+        self.x0 = self.x.copy()
+
+    def build_list(self):
+        pass
+
+
+def _worker(rank, world, port, q, skin=0.0):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -152,18 +186,18 @@ def _worker(rank, world, port, q):
 
     a = (4 / RHO) ** (1 / 3)
     L = [NUC * a] * 3
-    cells = [int(L[0] // 2.5)] * 3
+    cells = [int(L[0] // (2.5 + skin))] * 3
     x, y, z = O.fcc_positions([NUC] * 3, [a] * 3, L, 0.05, 42)
     vx, vy, vz = O.velocities(len(x), 0.722, 1.0, 42)
     layout = slab.SlabLayout(cells[0], world, rank)
-    eng = CpuSlabEngine(O, layout, cells, L)
+    eng = CpuVerletSlabEngine(O, layout, cells, L, skin) if skin else CpuSlabEngine(O, layout, cells, L)
     eng.load(np.stack([x, y, z], 1), np.stack([vx, vy, vz], 1), np.arange(len(x), dtype=np.int32))
     st = slab.SlabStep(eng, slab.NeighbourExchanger(layout))
     out = [st.start(energy=True)]
     f0 = (eng.id.copy(), eng.f.copy())
     for _ in range(NSTEPS):
         out.append(st.step(energy=True))
-    q.put((rank, out, f0, eng.id.copy(), eng.x.copy()))
+    q.put((rank, out, f0, eng.id.copy(), np.mod(eng.x, np.asarray(L)), st.rebuilds))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -176,12 +210,11 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_protocol_matches_single_domain(oracle, world):
+def _check(oracle, world, skin):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, skin)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -192,7 +225,7 @@ def test_slab_protocol_matches_single_domain(oracle, world):
     # single-domain reference
     a = (4 / RHO) ** (1 / 3)
     L = [NUC * a] * 3
-    cells = [int(L[0] // 2.5)] * 3
+    cells = [int(L[0] // (2.5 + skin))] * 3
     x, y, z = oracle.fcc_positions([NUC] * 3, [a] * 3, L, 0.05, 42)
     vx, vy, vz = oracle.velocities(len(x), 0.722, 1.0, 42)
     ref = oracle.md_run(x, y, z, vx, vy, vz, np.arange(len(x)), cells, L, NSTEPS)
@@ -215,12 +248,28 @@ def test_slab_protocol_matches_single_domain(oracle, world):
                                    for k in range(3)))
     assert res[0][1][0]["pairs"] == npair
     assert all(r[1][-1]["n"] == len(x) for r in res)
-    # final positions by id
+    # final positions by id (minimum image: a particle may sit on either side of a face)
     ids_f = np.concatenate([r[3] for r in res])
     xs_f = np.concatenate([r[4] for r in res])
     xref = np.empty_like(xs_f)
     xref[ref["id"]] = ref["x"]
-    assert np.abs(xs_f - xref[ids_f]).max() < 1e-11
+    d = xs_f - xref[ids_f]
+    d -= np.asarray(L) * np.rint(d / np.asarray(L))
+    assert np.abs(d).max() < 1e-11
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_protocol_matches_single_domain(oracle, world):
+    _check(oracle, world, 0.0)
+
+
+def test_verlet_slab_protocol(oracle):
+    """Verlet slabs over gloo: list rebuilds taken by both ranks together
+    (global max of the displacement flags), fixed-size ghost exchanges in
+    between, migration only at rebuilds."""
+    res = _check(oracle, 2, 0.12)
+    assert all(r[5] >= 2 for r in res)  # the initial build + at least one rebuild
 
 
 def test_layout_logic():
