@@ -293,6 +293,11 @@ int cs_pack_plane(const cs_box *b, int plane, const int32_t *cell_start, const d
                   const double *y, const double *z, double xshift, double *out, void *stream);
 int cs_add_plane_forces(const cs_box *b, int plane, const int32_t *cell_start, const double *in,
                         double *fx, double *fy, double *fz, void *stream);
+/* The same for a known particle range [lo, hi) (no host synchronisation). */
+int cs_pack_range(int64_t lo, int64_t hi, const double *x, const double *y, const double *z,
+                  double xshift, double *out, void *stream);
+int cs_add_range_forces(int64_t lo, int64_t hi, const double *in, double *fx, double *fy,
+                        double *fz, void *stream);
 
 /* Slab decomposition (x-slabs, one rank per GPU).  Packed rows
  * are [7][stride] doubles: x, y, z, vx, vy, vz, id.

@@ -110,6 +110,8 @@ _SIGS = {
     "cs_unpack7": (C.c_int, [_I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "cs_plane_counts": (C.c_int, [_P, C.c_int, _P, _P, _P, _P]),
     "cs_ghost_ws_bytes": (_SZ, [_P]),
+    "cs_pack_range": (C.c_int, [_I64, _I64, _P, _P, _P, _D, _P, _P]),
+    "cs_add_range_forces": (C.c_int, [_I64, _I64, _P, _P, _P, _P, _P]),
     "cs_set_ghost_plane": (C.c_int, [_P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
 }
 
@@ -167,10 +169,16 @@ def hptr(obj) -> C.c_void_p:
 
 
 def stream_handle(stream=None) -> C.c_void_p:
+    """cudaStream_t of `stream` or of torch's current stream on the current
+    device (raw-handle fast path: this sits in front of every kernel launch)."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return C.c_void_p(stream.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return C.c_void_p(raw(torch._C._cuda_getDevice()))
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def require_cuda():

@@ -384,6 +384,22 @@ extern "C" int cs_add_plane_forces(const cs_box *bx, int plane, const int32_t *c
   return cs_check_launch("add_plane_forces");
 }
 
+// the same for a known particle range [lo, hi) (no host synchronisation: a
+// Verlet slab between rebuilds keeps its plane ranges)
+extern "C" int cs_pack_range(int64_t lo, int64_t hi, const double *x, const double *y,
+                             const double *z, double xshift, double *out, void *stream) {
+  if (hi > lo)
+    k_pack_plane<<<grid_for(hi - lo, 256), 256, 0, cs_stream(stream)>>>(lo, hi, x, y, z, xshift, out);
+  return cs_check_launch("pack_range");
+}
+
+extern "C" int cs_add_range_forces(int64_t lo, int64_t hi, const double *in, double *fx,
+                                   double *fy, double *fz, void *stream) {
+  if (hi > lo)
+    k_add_plane<<<grid_for(hi - lo, 256), 256, 0, cs_stream(stream)>>>(lo, hi, in, fx, fy, fz);
+  return cs_check_launch("add_range_forces");
+}
+
 // ------------------------------------------------------- slab decomposition --
 // Particles are exchanged as packed rows [7][stride] of doubles:
 // x, y, z, vx, vy, vz, id (the id is exact in a double).

@@ -190,7 +190,7 @@ class SlabStep:
         # positions of my first plane go left; the right rank's first plane is my ghost
         if fixed:
             _, g_xyz_r = self.x.exchange_fixed(xyz, xyz[:0], 0, 3 * self.e.n_ghost)
-            self.e.set_ghosts(self._g_counts, g_xyz_r)
+            self.e.update_ghosts(g_xyz_r)
         else:
             g_counts_l, g_counts_r = self.x.exchange(counts, counts[:0])
             g_xyz_l, g_xyz_r = self.x.exchange(xyz, xyz[:0])
@@ -428,18 +428,17 @@ class CudaSlabEngine:
     def pack_first_plane(self, xshift, cached: bool = False):
         torch = _torch()
         if cached:  # Verlet between rebuilds: same cells, same particle range
-            m = self._first_m
+            lo, hi = self._first_range
         else:
             rng = (C.c_int64 * 2)()
             _lib.call("cs_plane_counts", C.byref(self.cbox), 0, _lib.ptr(self.cell_start),
                       _lib.ptr(self.counts), rng, self._s())
-            m = rng[1] - rng[0]
-            self._first_m = m
-        out = torch.empty(3 * m, dtype=torch.float64, device=self.device)
+            lo, hi = self._first_range = (rng[0], rng[1])
+        out = torch.empty(3 * (hi - lo), dtype=torch.float64, device=self.device)
         a = self.A
-        _lib.call("cs_pack_plane", C.byref(self.cbox), 0, _lib.ptr(self.cell_start), _lib.ptr(a["x"]),
-                  _lib.ptr(a["y"]), _lib.ptr(a["z"]), float(xshift), _lib.ptr(out), self._s())
-        return self.counts.to(torch.float64), out
+        _lib.call("cs_pack_range", lo, hi, _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]),
+                  float(xshift), _lib.ptr(out), self._s())
+        return (None if cached else self.counts.to(torch.float64)), out
 
     def set_ghosts(self, counts, xyz):
         torch = _torch()
@@ -453,6 +452,14 @@ class CudaSlabEngine:
                   _lib.ptr(a["y"]), _lib.ptr(a["z"]), _lib.ptr(a["fx"]), _lib.ptr(a["fy"]),
                   _lib.ptr(a["fz"]), _lib.ptr(self.ws), self.wsb, self._s())
         self.n_ghost = m
+
+    def update_ghosts(self, xyz):
+        """Verlet, between rebuilds: same ghost particles in the same slots --
+        overwrite their positions only (no cell-list work, no host sync)."""
+        m, o, a = self.n_ghost, self.n_owned, self.A
+        xyz = xyz.view(3, m)
+        for k, key in enumerate(("x", "y", "z")):
+            a[key][o:o + m].copy_(xyz[k])
 
     def forces(self, energy, sync: bool = True):
         """Local forces.  sync=False (Verlet, between rebuilds, no energy): no
@@ -483,18 +490,19 @@ class CudaSlabEngine:
         return float(self.scal[0].item()) if energy else 0.0, int(self.npairs.item())
 
     def pack_ghost_forces(self):
+        """Ghost-plane forces (the ghost plane is the array tail [n_owned, n_owned + n_ghost))."""
         torch = _torch()
         out = torch.empty(3 * self.n_ghost, dtype=torch.float64, device=self.device)
         a = self.A
-        _lib.call("cs_pack_plane", C.byref(self.cbox), self.cbox.nc[0] - 1, _lib.ptr(self.cell_start),
-                  _lib.ptr(a["fx"]), _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), 0.0, _lib.ptr(out), self._s())
+        _lib.call("cs_pack_range", self.n_owned, self.n_owned + self.n_ghost, _lib.ptr(a["fx"]),
+                  _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), 0.0, _lib.ptr(out), self._s())
         return out
 
     def add_first_plane_forces(self, f):
         a = self.A
-        _lib.call("cs_add_plane_forces", C.byref(self.cbox), 0, _lib.ptr(self.cell_start),
-                  _lib.ptr(f.to(self.device)), _lib.ptr(a["fx"]), _lib.ptr(a["fy"]), _lib.ptr(a["fz"]),
-                  self._s())
+        lo, hi = self._first_range  # set by pack_first_plane in the same force evaluation
+        _lib.call("cs_add_range_forces", lo, hi, _lib.ptr(f.to(self.device)), _lib.ptr(a["fx"]),
+                  _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), self._s())
 
     def kinetic(self):
         a = self.A

@@ -111,6 +111,9 @@ class CpuSlabEngine:
         self.gcount = counts.numpy().astype(int)
         self.n_ghost = len(self.gx)
 
+    def update_ghosts(self, xyz):
+        self.gx = xyz.numpy().reshape(3, -1).T.copy()
+
     def forces(self, energy, sync=True):
         O = self.O
         ny, nz = self.cells[1], self.cells[2]
