@@ -109,3 +109,19 @@ def test_verlet_needs_wide_cells(cuda):
     box, nuc, a = md.fcc_box(14, 0.8442)  # cells of edge >= rc only
     with pytest.raises(ValueError):
         md.LJSystem(box, 4 * 14 ** 3, schedule="verlet", skin=0.3)
+
+
+def test_verlet_crowded_cell_is_reported(cuda):
+    """A home cell with more than 32 particles cannot be laid out on a warp's
+    lanes: the build flags it and the system raises instead of returning
+    partial forces."""
+    rng = np.random.default_rng(5)
+    box = md.LJBox((24.0, 24.0, 24.0), (8, 8, 8))  # edge 3.0 >= rc + skin
+    n = 3000
+    pts = rng.random((n, 3)) * 24.0
+    pts[:60] = 0.2 + rng.random((60, 3)) * 2.5  # 60 particles in one cell
+    s = md.LJSystem(box, n, schedule="verlet", skin=0.3)
+    z = np.zeros(n)
+    s.load_host(pts[:, 0], pts[:, 1], pts[:, 2], z, z, z, np.arange(n))
+    with pytest.raises(Exception, match="more than 32 particles"):
+        s.energies()
