@@ -73,10 +73,6 @@ struct ShellSmem : ShellBase<SH_RCAP, SH_HCAP> {  // link-cell super-tasks
 };
 struct ShellSmemVL : ShellBase<VL_RCAP, VL_HCAP> {};  // Verlet round tables
 
-__device__ __forceinline__ double box_d2(double x, double lo, double hi) {
-  const double d = fmax(fmax(lo - x, 0.0), x - hi);
-  return d * d;
-}
 
 // 1/a to ~1 ulp: hardware approximation + two Newton-Raphson steps
 __device__ __forceinline__ double fast_rcp(double a) {
@@ -499,8 +495,6 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   for (int i = threadIdx.x; i < RCAP + HCAP; i += blockDim.x) S.RF[0][i] = S.RF[1][i] = S.RF[2][i] = 0.0;
   __syncthreads();
 
-  const double edge0 = b.L[0] / b.gnc[0], edge1 = b.L[1] / b.gnc[1], edge2 = b.L[2] / b.gnc[2];
-  const double cull2 = A.p.rc2 * (1.0 + 1e-12) + 1e-12;
   const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
   // ---- 1-4. one warp per home cell
   if constexpr (VERLET) {
@@ -508,9 +502,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   } else {
   for (int h = wid; h < nhome; h += SH_NW) {
     if (S.hcell[h] < 0) continue;
-    const int hg0 = o0[0] + h % B0, hg1 = o0[1] + (h / B0) % B1, hg2 = o0[2] + h / (B0 * B1);
     const int a0 = S.sstart[h][0], na = S.scount[h][0];
-    (void)hg0; (void)hg1; (void)hg2; (void)cull2; (void)edge0; (void)edge1; (void)edge2;
     // 1. j list = the 14 source cells concatenated (home first).  Lanes walk
     //    the concatenation directly (no per-cell partial warps); a box-distance
     //    cull was measured to cost more than the candidates it removes.
