@@ -50,7 +50,7 @@ struct MergeTable {              // host-built per block shape
   int nfc;
 };
 
-template <int RCAP_, int HCAP_>
+template <int RCAP_, int HCAP_, int QN>
 struct ShellBase {
   static constexpr int RCAP = RCAP_, HCAP = HCAP_;
   double RF[3][RCAP + HCAP];         // reaction slots (e >= 1), then home rows (e = 0)
@@ -62,16 +62,19 @@ struct ShellBase {
   int fgstart[SH_MAXF];              // footprint cell -> global start (-1: none)
   int hcell[SH_MAXB];
   int16_t mt_base[SH_MAXF][SH_MAXC];  // merge: slot base of each contributor (-1: home not owned)
+  int pend[QN];                    // Verlet: contributing homes still running per footprint cell
+  int queue[QN];                   // Verlet: footprint cells ready to merge, in order (-1: not yet)
+  int qtail, qhead;
   int overflow;
   uint8_t mt_n[SH_MAXF];           // merge-table counts in shared memory (lanes of one warp
                                    //   read different cells: divergent constant reads serialise)
 };
-struct ShellSmem : ShellBase<SH_RCAP, SH_HCAP> {  // link-cell super-tasks
+struct ShellSmem : ShellBase<SH_RCAP, SH_HCAP, 1> {  // link-cell super-tasks
   double rows[SH_NW][SH_IB][3][32];  // per-lane i partials
   double hx[SH_NW][SH_IB][4];        // broadcast home positions
   uint16_t jl[SH_NW][SH_JCAP];       // j list: entry << 12 | index in source cell
 };
-struct ShellSmemVL : ShellBase<VL_RCAP, VL_HCAP> {};  // Verlet round tables
+struct ShellSmemVL : ShellBase<VL_RCAP, VL_HCAP, SH_MAXF> {};  // Verlet round tables
 
 
 // 1/a to ~1 ulp: hardware approximation + two Newton-Raphson steps
@@ -224,13 +227,15 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, i
   }
 }
 
-// lanes of one home particle are contiguous: segmented reduction, then the
-// first lane of each run adds the particle's F_i into its home row
+// lanes whose FIRST particle is p are contiguous and at most VB_SEG (4) long:
+// a two-step segmented reduction, then the first lane of each run adds the
+// particle's F_i into its home row.  A particle is the SECOND particle of at
+// most one lane, so those partials are added directly, after the first ones.
 template <class SM>
 __device__ __forceinline__ void verlet_fi(SM &S, int h, int lane, int im, double fix, double fiy,
-                                          double fiz) {
+                                          double fiz, int im2, double fbx, double fby, double fbz) {
 #pragma unroll
-  for (int s = 1; s < 32; s <<= 1) {
+  for (int s = 1; s < 4; s <<= 1) {
     const double ux = __shfl_down_sync(CS_FULL, fix, s);
     const double uy = __shfl_down_sync(CS_FULL, fiy, s);
     const double uz = __shfl_down_sync(CS_FULL, fiz, s);
@@ -249,6 +254,21 @@ __device__ __forceinline__ void verlet_fi(SM &S, int h, int lane, int im, double
     S.RF[2][slot] += fiz;
   }
   __syncwarp();
+  if (im2 != 0xFF) {
+    const int slot = S.sbase[h][0] + im2;
+    S.RF[0][slot] += fbx;
+    S.RF[1][slot] += fby;
+    S.RF[2][slot] += fbz;
+  }
+  __syncwarp();
+}
+
+// footprint cell of stencil entry e of home h (block-local coordinates, the
+// merge table's numbering)
+__device__ __forceinline__ int foot_of(const Box &b, int h, int e) {
+  const int B0 = b.blk[0], B1 = b.blk[1], FX = B0 + 1, FY = B1 + 2;
+  return (h % B0 + c_stencil3.o[e][0]) + FX * (((h / B0) % B1 + c_stencil3.o[e][1] + 1) +
+                                               FY * (h / (B0 * B1) + c_stencil3.o[e][2] + 1));
 }
 
 template <bool ENERGY, class SM>
@@ -271,8 +291,17 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
       verlet_table<ENERGY, true>(S, A, h, S.sstart[h][0], dp, nr, pA, pB, sw, fa, fb, pe, hits);
     else
       verlet_table<ENERGY, false>(S, A, h, S.sstart[h][0], dp, nr, pA, pB, sw, fa, fb, pe, hits);
-    verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2]);
-    verlet_fi(S, h, lane, pB, fb[0], fb[1], fb[2]);
+    verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2], pB, fb[0], fb[1], fb[2]);
+    // this home's slots are final: count it off its 14 footprint cells; the
+    // last contributor of a cell queues it for merging
+    __threadfence_block();
+    if (lane < 14) {
+      const int lc = foot_of(A.b, h, lane);
+      if (atomicSub(&S.pend[lc], 1) == 1) {
+        const int q = atomicAdd(&S.qtail, 1);
+        atomicExch(&S.queue[q], lc);
+      }
+    }
     hits = warp_sum(hits);
     if (ENERGY) pe = warp_sum(pe);
     if (lane == 0) {
@@ -298,6 +327,70 @@ struct ShellArgs {
   int coff[9];            // dataflow mode: first ticket of each colour
   const unsigned char *vtab;  // Verlet mode: per-block tables cached at the list build
 };
+
+template <int MODE>
+__device__ __forceinline__ void merge_store(const ShellArgs &SA, int64_t o, int g, double sx,
+                                            double sy, double sz) {
+  const ForceArgs &A = SA.A;
+  if (MODE == SH_BUFFERED) {
+    SA.buf[o] = sx;
+    SA.buf[SA.bufstride + o] = sy;
+    SA.buf[2 * SA.bufstride + o] = sz;
+  } else if (MODE == SH_DATAFLOW) {  // other SMs wrote f: read through L2
+    A.fx[g] = __ldcg(A.fx + g) + sx;
+    A.fy[g] = __ldcg(A.fy + g) + sy;
+    A.fz[g] = __ldcg(A.fz + g) + sz;
+  } else {
+    A.fx[g] += sx;
+    A.fy[g] += sy;
+    A.fz[g] += sz;
+  }
+}
+
+// merge of footprint cell lc by one warp: home rows + reaction slots in the
+// fixed merge-table order, into the block buffer or f
+template <int MODE, class SM>
+__device__ __forceinline__ void merge_cell(const ShellArgs &SA, SM &S, int lc, int lane,
+                                           int64_t boff) {
+  const int g0 = S.fgstart[lc];
+  if (g0 < 0) return;
+  const int f0 = S.fstart[lc], n = S.fstart[lc + 1] - f0;
+  const int nc = S.mt_n[lc];
+  for (int i = lane; i < n; i += 32) {
+    double sx = 0, sy = 0, sz = 0;
+    for (int k = 0; k < nc; ++k) {
+      const int base = S.mt_base[lc][k];
+      if (base < 0) continue;
+      const int s = base + i;
+      sx += S.RF[0][s];
+      sy += S.RF[1][s];
+      sz += S.RF[2][s];
+    }
+    merge_store<MODE>(SA, boff + f0 + i, g0 + i, sx, sy, sz);
+  }
+}
+
+// Verlet mode, step 5 without a block barrier: warps that are done take
+// footprint cells from the ready queue in order and merge them while the
+// other homes are still running
+template <int MODE, class SM>
+__device__ __forceinline__ void verlet_merge_queue(const ShellArgs &SA, SM &S, int lane, int nfc,
+                                                   int64_t boff) {
+  while (true) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(&S.qhead, 1);
+    t = __shfl_sync(CS_FULL, t, 0);
+    if (t >= nfc) break;
+    int lc = -1;
+    if (lane == 0) {
+      volatile int *qv = S.queue;
+      while ((lc = qv[t]) < 0) __nanosleep(32);
+    }
+    lc = __shfl_sync(CS_FULL, lc, 0);
+    __threadfence_block();
+    merge_cell<MODE>(SA, S, lc, lane, boff);
+  }
+}
 
 // block coordinates -> global cell of a footprint cell (or -1)
 __device__ __forceinline__ int64_t foot_cell(const Box &b, const int *o0, int lc, int FX, int FY) {
@@ -404,15 +497,31 @@ __device__ __forceinline__ void shell_tables(const ShellArgs &SA, SM &S, const i
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < nfc * SH_MAXC; t += blockDim.x) {
-    const int lc = t / SH_MAXC, k = t - SH_MAXC * (t / SH_MAXC);
-    int base = -1;
-    if (k < SA.mt.n[lc]) {
-      const int he = SA.mt.he[lc][k];
-      const int hh = he >> 4, e = he & 15;
-      if (S.hcell[hh] >= 0) base = S.sbase[hh][e];
+  for (int lc = threadIdx.x; lc < SH_MAXF; lc += blockDim.x) {
+    int live = 0;
+#pragma unroll
+    for (int k = 0; k < SH_MAXC; ++k) {
+      int base = -1;
+      if (lc < nfc && k < SA.mt.n[lc]) {
+        const int he = SA.mt.he[lc][k];
+        const int hh = he >> 4, e = he & 15;
+        if (S.hcell[hh] >= 0) base = S.sbase[hh][e];
+      }
+      if (lc < nfc) S.mt_base[lc][k] = (int16_t)base;
+      live += base >= 0;
     }
-    S.mt_base[lc][k] = (int16_t)base;
+    if (VERLET) {
+      S.pend[lc] = live;
+      S.queue[lc] = -1;
+    }
+  }
+  __syncthreads();
+  if (VERLET && threadIdx.x == 0) {  // cells nobody writes are ready from the start
+    int n0 = 0;
+    for (int lc = 0; lc < nfc; ++lc)
+      if (S.pend[lc] == 0) S.queue[n0++] = lc;
+    S.qtail = n0;
+    S.qhead = 0;
   }
   __syncthreads();
 }
@@ -645,6 +754,13 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     }
   }
   }  // link-cell super-tasks
+  if constexpr (VERLET) {
+    verlet_merge_queue<MODE>(SA, S, lane, nfc, BUFFERED ? SA.boff[bid] : 0);
+    if (BUFFERED)
+      for (int lc = threadIdx.x; lc <= nfc; lc += blockDim.x)
+        SA.bindex[(int64_t)bid * (SH_MAXF + 1) + lc] = S.fstart[lc];
+    return;
+  }
   __syncthreads();
   // ---- 5. merge, one thread per footprint particle: home rows + reaction
   //         slots in the fixed merge-table order
