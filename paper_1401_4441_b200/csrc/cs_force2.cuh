@@ -147,30 +147,77 @@ __device__ __forceinline__ void verlet_react(SM &S, int slot, double fx, double 
   dst[2 * stride] = c - fz;
 }
 
+// Per-warp home data loaded at block start, before the table copy lands, so
+// their latency overlaps the prologue: lane map, round count, the first four
+// descriptors, then (after the copy) the lane's home particle positions.
+struct VPre {
+  int cell, nr, pA, pB, sw, a0;
+  unsigned d0, d1, d2, d3;
+  double xi, yi, zi, xb, yb, zb;
+};
+
+__device__ __forceinline__ void vl_pre_issue(const ForceArgs &A, const int *o0, int wid, int lane,
+                                             VPre &v) {
+  const Box &b = A.b;
+  const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
+  v.cell = -1;
+  v.nr = 0;
+  v.pA = v.pB = 0xFF;
+  v.sw = 0;
+  v.a0 = 0;
+  v.d0 = v.d1 = v.d2 = v.d3 = VL_IDLE;
+  if (wid >= B0 * B1 * B2) return;
+  const int hg0 = o0[0] + wid % B0, hg1 = o0[1] + (wid / B0) % B1, hg2 = o0[2] + wid / (B0 * B1);
+  if (hg0 >= b.owned_x) return;
+  v.cell = (int)box_cell(b, hg0, hg1, hg2);
+  v.nr = __ldg(A.vl_nround + v.cell);
+  const uint8_t *lm = A.vl_imap + (int64_t)v.cell * 96;
+  v.pA = __ldg(lm + lane);
+  v.pB = __ldg(lm + 32 + lane);
+  v.sw = __ldg(lm + 64 + lane);
+  const uint16_t *dp = A.vl_desc + (int64_t)v.cell * (VL_RMAX * 32) + lane;
+  v.d0 = __ldg(dp);
+  v.d1 = __ldg(dp + 32);
+  v.d2 = __ldg(dp + 64);
+  v.d3 = __ldg(dp + 96);
+  v.a0 = __ldg(A.start + v.cell);
+}
+
+__device__ __forceinline__ void vl_pre_positions(const ForceArgs &A, VPre &v) {
+  v.xi = v.yi = v.zi = v.xb = v.yb = v.zb = 0.0;
+  if (v.cell < 0) return;
+  if (v.nr < 4) {  // rounds past the table are idle
+    if (v.nr < 1) v.d0 = VL_IDLE;
+    if (v.nr < 2) v.d1 = VL_IDLE;
+    if (v.nr < 3) v.d2 = VL_IDLE;
+    v.d3 = VL_IDLE;
+  }
+  if (v.pA != 0xFF) {
+    v.xi = __ldg(A.x + v.a0 + v.pA);
+    v.yi = __ldg(A.y + v.a0 + v.pA);
+    v.zi = __ldg(A.z + v.a0 + v.pA);
+  }
+  if (v.pB != 0xFF) {
+    v.xb = __ldg(A.x + v.a0 + v.pB);
+    v.yb = __ldg(A.y + v.a0 + v.pB);
+    v.zb = __ldg(A.z + v.a0 + v.pB);
+  }
+}
+
 // Rounds are taken in pairs (the builder aligns switch rounds to even): the
 // two pairs of a lane are independent chains (ILP); their reactions are
 // written round by round, each round's j being distinct.  Descriptors are
 // prefetched two rounds ahead of the pair being computed, positions one.
 template <bool ENERGY, bool SHIFT, class SM>
-__device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, int a0,
-                                             const uint16_t *dp, int nr, int pA, int pB, int sw,
-                                             double *fa, double *fb, double &pe,
-                                             unsigned &hits) {
-  double xi = 0, yi = 0, zi = 0, xb = 0, yb = 0, zb = 0;
-  if (pA != 0xFF) {
-    xi = __ldg(A.x + a0 + pA);
-    yi = __ldg(A.y + a0 + pA);
-    zi = __ldg(A.z + a0 + pA);
-  }
-  if (pB != 0xFF) {
-    xb = __ldg(A.x + a0 + pB);
-    yb = __ldg(A.y + a0 + pB);
-    zb = __ldg(A.z + a0 + pB);
-  }
+__device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, const VPre &v,
+                                             const uint16_t *dp, double *fa, double *fb,
+                                             double &pe, unsigned &hits) {
+  const int nr = v.nr, sw = v.sw;
+  double xi = v.xi, yi = v.yi, zi = v.zi;
+  const double xb = v.xb, yb = v.yb, zb = v.zb;
   double fx_ = 0, fy_ = 0, fz_ = 0;
   // idle slots (entry 15) read a real particle and never pass the r^2 test
-  unsigned d0 = nr > 0 ? __ldg(dp) : VL_IDLE, d1 = nr > 1 ? __ldg(dp + 32) : VL_IDLE;
-  unsigned d2 = nr > 2 ? __ldg(dp + 64) : VL_IDLE, d3 = nr > 3 ? __ldg(dp + 96) : VL_IDLE;
+  unsigned d0 = v.d0, d1 = v.d1, d2 = v.d2, d3 = v.d3;
   int g = S.sstart[h][d0 >> 8] + (d0 & 255);
   double x0 = __ldg(A.x + g), y0 = __ldg(A.y + g), z0 = __ldg(A.z + g);
   g = S.sstart[h][d1 >> 8] + (d1 & 255);
@@ -271,15 +318,14 @@ __device__ __forceinline__ int foot_of(const Box &b, int h, int e) {
                                                FY * (h / (B0 * B1) + c_stencil3.o[e][2] + 1));
 }
 
+// one home cell per warp (blocks have at most SH_NW = 8 cells)
 template <bool ENERGY, class SM>
 __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lane, int wid,
-                                              int nhome) {
-  for (int h = wid; h < nhome; h += SH_NW) {
-    const int cell = S.hcell[h];
-    if (cell < 0) continue;
-    const uint8_t *lm = A.vl_imap + (int64_t)cell * 96;
-    const int nr = A.vl_nround[cell];
-    const int pA = lm[lane], pB = lm[32 + lane], sw = lm[64 + lane];
+                                              const VPre &v) {
+  {
+    const int h = wid, cell = v.cell;
+    if (cell < 0) return;
+    const int pA = v.pA, pB = v.pB;
     double pe = 0;
     unsigned hits = 0;
     double fa[3] = {0, 0, 0}, fb[3] = {0, 0, 0};
@@ -288,13 +334,13 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
                                                          S.sh[h][lane < 14 ? lane : 0][1] != 0.0 ||
                                                          S.sh[h][lane < 14 ? lane : 0][2] != 0.0));
     if (shift)
-      verlet_table<ENERGY, true>(S, A, h, S.sstart[h][0], dp, nr, pA, pB, sw, fa, fb, pe, hits);
+      verlet_table<ENERGY, true>(S, A, h, v, dp, fa, fb, pe, hits);
     else
-      verlet_table<ENERGY, false>(S, A, h, S.sstart[h][0], dp, nr, pA, pB, sw, fa, fb, pe, hits);
+      verlet_table<ENERGY, false>(S, A, h, v, dp, fa, fb, pe, hits);
     verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2], pB, fb[0], fb[1], fb[2]);
     // this home's slots are final: count it off its 14 footprint cells; the
     // last contributor of a cell queues it for merging
-    __threadfence_block();
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
     if (lane < 14) {
       const int lc = foot_of(A.b, h, lane);
       if (atomicSub(&S.pend[lc], 1) == 1) {
@@ -387,7 +433,7 @@ __device__ __forceinline__ void verlet_merge_queue(const ShellArgs &SA, SM &S, i
       while ((lc = qv[t]) < 0) __nanosleep(32);
     }
     lc = __shfl_sync(CS_FULL, lc, 0);
-    __threadfence_block();
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
     merge_cell<MODE>(SA, S, lc, lane, boff);
   }
 }
@@ -558,12 +604,21 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   const int nfc = SA.mt.nfc;
 
   bool cached = false;
+  VPre pre;
   if constexpr (VERLET) {
-    if (SA.vtab) {  // tables cached at the list build: 16-byte copy into shared memory
+    vl_pre_issue(A, o0, wid, lane, pre);
+    if (SA.vtab) {  // tables cached at the list build: asynchronous 16-byte copies into
+                    // shared memory while the reaction slots are zeroed
       const int blin = o0[0] / B0 + A.nbk[0] * (o0[1] / B1 + A.nbk[1] * (o0[2] / B2));
-      const int4 *src = reinterpret_cast<const int4 *>(SA.vtab + (size_t)blin * vl_table_bytes());
-      int4 *dst = reinterpret_cast<int4 *>(reinterpret_cast<unsigned char *>(&S) + offsetof(SM, sh));
-      for (int k = threadIdx.x; k < (int)(vl_table_bytes() / 16); k += blockDim.x) dst[k] = __ldg(src + k);
+      const unsigned char *src = SA.vtab + (size_t)blin * vl_table_bytes();
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(reinterpret_cast<unsigned char *>(&S) +
+                                                              offsetof(SM, sh));
+      for (int k = threadIdx.x; k < (int)(vl_table_bytes() / 16); k += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * k), "l"(src + 16 * k)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      for (int i = threadIdx.x; i < RCAP + HCAP; i += blockDim.x) S.RF[0][i] = S.RF[1][i] = S.RF[2][i] = 0.0;
+      asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       cached = true;
     }
@@ -601,13 +656,15 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
     return;
     }
   }
-  for (int i = threadIdx.x; i < RCAP + HCAP; i += blockDim.x) S.RF[0][i] = S.RF[1][i] = S.RF[2][i] = 0.0;
+  if (VERLET) vl_pre_positions(A, pre);
+  if (!cached)
+    for (int i = threadIdx.x; i < RCAP + HCAP; i += blockDim.x) S.RF[0][i] = S.RF[1][i] = S.RF[2][i] = 0.0;
   __syncthreads();
 
   const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
   // ---- 1-4. one warp per home cell
   if constexpr (VERLET) {
-    verlet_rounds<ENERGY>(S, A, lane, wid, nhome);
+    verlet_rounds<ENERGY>(S, A, lane, wid, pre);
   } else {
   for (int h = wid; h < nhome; h += SH_NW) {
     if (S.hcell[h] < 0) continue;
