@@ -223,6 +223,7 @@ __device__ __forceinline__ void verlet_table(SM &S, const ForceArgs &A, int h, c
   g = S.sstart[h][d1 >> 8] + (d1 & 255);
   double x1 = __ldg(A.x + g), y1 = __ldg(A.y + g), z1 = __ldg(A.z + g);
   dp += 128;
+#pragma unroll 2
   for (int r = 0; r < nr; r += 2) {
     if (r == sw) {  // this lane continues with its second particle
       fa[0] = fx_;
