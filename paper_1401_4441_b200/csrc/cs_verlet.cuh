@@ -342,9 +342,12 @@ __global__ void __launch_bounds__(VB_NW * 32) k_verlet_build(Box b, const int32_
           ++Lc;
           off = segs = 0;
         }
-        if (rest > 0) {
-          Lc += rest / R;
-          off = rest % R;
+        if (rest > 0) {  // (rest < VB_SEG * R: a short loop, no integer division)
+          while (rest >= R) {
+            rest -= R;
+            ++Lc;
+          }
+          off = rest;
           segs = off ? 1 : 0;
         }
       }
