@@ -502,7 +502,60 @@ def run_ours(args):
                         + (m["builds"] or 0) * getattr(sysm, "REBUILD_LAUNCHES", 0),
         "clocks": m["clocks"],
     }
+    if ws == 1 and args.config == "cfg2" and not args.no_schedule:
+        line["schedule_analysis"] = schedule_report(torch, cpu=not args.no_cpu)
     print(json.dumps(line), flush=True)
+
+
+SCHED_GRIDS = {"cfg1": (4, 4, 4), "cfg5": (64, 64, 192)}
+SCHED_ORDERS = (("lexicographic", "basic", 2), ("colour 2x2x2", "loopex", 2), ("colour 3x3x3", "loopex", 3))
+
+
+def schedule_report(torch, cpu=True):
+    """BASELINE cfg1/cfg5 serialization analysis (K4): generate the task
+    stream, detect its inout dependencies and take the critical path, all on
+    the device -- the reference pipeline generate -> detect_dependencies ->
+    critical_path (taskgen.py:180-234, depgraph.py:102-174).  Device wall time
+    per order (after one warm-up) next to the oracle's C port of the same
+    pipeline on one host core."""
+    from paper_1401_4441_b200 import GridSpec, schedule
+
+    out = {}
+    for cname, ext in SCHED_GRIDS.items():
+        g = GridSpec(ext)
+        rows = {}
+        for label, strat, stride in SCHED_ORDERS:
+            if cname == "cfg1" and stride == 3:
+                continue  # (4 is not a multiple of 3)
+            schedule.device_stream(g, strat, stride=stride).depth()  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ds = schedule.device_stream(g, strat, stride=stride)
+            ne = ds.edges()[2]
+            d = ds.depth()
+            torch.cuda.synchronize()
+            t_dev = time.perf_counter() - t0
+            row = {"tasks": ds.ntasks, "edges": ne, "depth": d,
+                   "degree_of_serialization": ds.ntasks / d, "device_ms": 1e3 * t_dev}
+            del ds
+            if cpu:
+                from oracle import oracle as O
+                from paper_1401_4441_b200.taskgen import StencilOrder
+                t0 = time.perf_counter()
+                if strat == "basic":
+                    h, nb, _ = O.stream_basic(ext, (1, 1, 1), StencilOrder.canonical(3).offsets)
+                else:
+                    h, nb, _ = O.stream_loopex(ext, (1, 1, 1), stride)
+                eu, ev = O.detect_edges_stream(h, nb)
+                dc = O.critical_path(len(h), eu, ev)
+                row["cpu_port_ms"] = 1e3 * (time.perf_counter() - t0)
+                row["cpu_port_depth"] = int(dc)
+                del h, nb, eu, ev
+            rows[label] = row
+        out[cname] = {"grid": list(ext), "orders": rows}
+    out["note"] = ("device: stream generation + edge detection + critical path (wall clock incl. "
+                   "allocations); cpu_port: oracle/cs_oracle.c restatement of the same pipeline, 1 core")
+    return out
 
 
 def e2e_run(torch, md, ref_sys, args):
@@ -559,6 +612,7 @@ def main():
     ap.add_argument("--skin", type=float, default=0.35, help="Verlet skin (verlet schedules)")
     ap.add_argument("--block", type=lambda s: tuple(int(v) for v in s.split(",")), default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-schedule", action="store_true", help="skip the cfg1/cfg5 serialization analysis")
     ap.add_argument("--slab", action="store_true", help="use the x-slab engine even at N=1")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

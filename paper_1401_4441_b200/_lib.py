@@ -124,7 +124,8 @@ def load(path: str | None = None):
     """Load the shared library (raises if it was not built)."""
     global _lib
     if _lib is None:
-        p = path or LIB
+        # (CELLSCHED_B200_LIB: load a differently built copy, for kernel experiments)
+        p = path or os.environ.get("CELLSCHED_B200_LIB") or LIB
         if not os.path.exists(p):
             raise ImportError(
                 f"{p} not found: build it with `python -m paper_1401_4441_b200._build` "

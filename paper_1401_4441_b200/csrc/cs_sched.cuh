@@ -467,6 +467,94 @@ __global__ void k_depth_chain(int64_t ncells, const int32_t *first, const int32_
   (void)home;
 }
 
+// (c) the same DP for a fully periodic cell-grouped stream, with the state
+//     vector in shared memory.  Cells are visited plane by plane along the
+//     slowest axis; a cell's tasks touch only planes z-1, z, z+1, so a ring
+//     of three planes (slot q % 3) plus a fixed slot for the last plane (the
+//     periodic image of plane -1) holds every live state.  Plane 0 is parked
+//     in global memory when it leaves the ring and brought back for the last
+//     plane (its +1 neighbour).  Per cell, lanes hold the tasks in stream
+//     order and the chain L_e = 1 + max(L_{e-1}, s[n_e]) is evaluated in
+//     closed form, L_e = e + 1 + max(s[home], max_{k<=e}(s[n_k] - k)), by one
+//     warp prefix-max; the entry offsets come from cell 0's neighbours.
+//     Requires every extent >= 3 (distinct neighbours within a cell).
+__global__ void __launch_bounds__(32) k_depth_planes(int ex, int ey, int ez, int n,
+                                                     const int32_t *nbr, int32_t *level,
+                                                     int32_t *parked, int32_t *depth) {
+  extern __shared__ int32_t win[];  // 4 slots of ex * ey states
+  const int lane = threadIdx.x;
+  const int P = ex * ey;
+  // entry offsets from cell 0's tasks (nbr = -1 or 0: intra)
+  int ox = 0, oy = 0, oz = 0;
+  bool inter = false;
+  if (lane < n) {
+    const int nb = nbr[lane];
+    if (nb > 0) {
+      inter = true;
+      const int nx = nb % ex, ny = (nb / ex) % ey, nz = nb / P;
+      ox = nx == 0 ? 0 : (nx == 1 ? 1 : -1);
+      oy = ny == 0 ? 0 : (ny == 1 ? 1 : -1);
+      oz = nz == 0 ? 0 : (nz == 1 ? 1 : -1);
+    }
+  }
+  for (int i = lane; i < 4 * P; i += 32) win[i] = 0;
+  bool parked0 = false;
+  int32_t best = 0;
+  int64_t c = 0;
+  __syncwarp();
+  for (int z = 0; z < ez; ++z) {
+    const int q = z + 1;  // plane entering the ring
+    if (z >= 1 && q <= ez - 2 && q >= 3) {
+      int32_t *slot = win + (q % 3) * P;  // held plane q - 3 = z - 2
+      if (z - 2 == 0) {
+        for (int i = lane; i < P; i += 32) parked[i] = slot[i];
+        parked0 = true;
+      }
+      for (int i = lane; i < P; i += 32) slot[i] = 0;
+    }
+    if (z == ez - 1 && parked0) {
+      int32_t *slot = win + (ez % 3) * P;
+      for (int i = lane; i < P; i += 32) slot[i] = parked[i];
+    }
+    __syncwarp();
+    // slot of plane z + oz for this lane's entry
+    const int pz = z + oz < 0 ? ez - 1 : (z + oz >= ez ? 0 : z + oz);
+    const int sl = pz == ez - 1 ? 3 : ((pz == 0 && z == ez - 1 && parked0) ? ez % 3 : pz % 3);
+    int32_t *base = win + sl * P;
+    int32_t *hbase = win + (z == ez - 1 ? 3 : z % 3) * P;
+    for (int y = 0; y < ey; ++y) {
+      int ny = y + oy;
+      ny = ny < 0 ? ny + ey : (ny >= ey ? ny - ey : ny);
+      const int rowo = ex * ny;
+      for (int x = 0; x < ex; ++x, ++c) {
+        int nx = x + ox;
+        nx = nx < 0 ? nx + ex : (nx >= ex ? nx - ex : nx);
+        const int a = rowo + nx;
+        const int32_t sh = hbase[x + ex * y];
+        int32_t w = inter ? base[a] - lane : INT32_MIN / 2;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          if (d >= n) break;
+          const int32_t u = __shfl_up_sync(CS_FULL, w, d);
+          if (lane >= d) w = max(w, u);
+        }
+        const int32_t L = lane + 1 + max(sh, w);
+        if (lane < n) {
+          level[c * n + lane] = L;
+          if (inter) base[a] = L;
+          if (lane == n - 1) {
+            hbase[x + ex * y] = L;
+            best = max(best, L);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  best = max(best, __shfl_sync(CS_FULL, best, n - 1));
+  if (lane == 0) *depth = best;
+}
+
 __global__ void k_cell_first_from_home(int64_t nt, const int32_t *home, int64_t ncells,
                                        int32_t *first) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt;
@@ -513,7 +601,25 @@ extern "C" int cs_stream_depth(const cs_grid *g, int strategy, int n, int64_t nt
   if (method == 2) method = strategy == CS_STREAM_BASIC ? 1 : 0;
   cs_ws w(ws, ws_bytes);
   CS_WS_TAKE(w, int32_t, scalars, 16);
-  if (method == 1) {
+  // plane-ring fast path: fully periodic, every extent >= 3, <= 32 entries
+  // per cell, every cell complete, four planes of states in shared memory
+  int e3[3] = {g->ext[0], g->dim == 3 ? g->ext[1] : 1, g->ext[g->dim - 1]};
+  bool ring = method == 1 && strategy == CS_STREAM_BASIC && (g->dim == 2 || g->dim == 3);
+  for (int k = 0; k < g->dim; ++k) ring = ring && g->periodic[k] && g->ext[k] >= 3;
+  const int nper = ncells > 0 ? (int)(ntasks / ncells) : 0;
+  ring = ring && nper >= 1 && nper <= 32 && (int64_t)nper * ncells == ntasks;
+  const size_t ring_smem = 4 * sizeof(int32_t) * (size_t)e3[0] * e3[1];
+  ring = ring && ring_smem <= 200 * 1024;
+  if (ring) {
+    CS_WS_TAKE(w, int32_t, parked, (int64_t)e3[0] * e3[1]);
+    static bool attr = false;
+    if (!attr) {
+      CS_CUDA(cudaFuncSetAttribute(k_depth_planes, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    k_depth_planes<<<1, 32, ring_smem, st>>>(e3[0], e3[1], e3[2], nper, nbr, level, parked, scalars);
+    CS_TRY(cs_check_launch("depth_planes"));
+  } else if (method == 1) {
     CS_REQUIRE(strategy == CS_STREAM_BASIC, "chain depth needs a cell-grouped (basic) stream");
     CS_WS_TAKE(w, int32_t, first, ncells + 1);
     CS_WS_TAKE(w, int32_t, s, ncells);

@@ -100,3 +100,24 @@ def test_edges_match_oracle_random_orders(oracle, cuda):
         deu, dev = s.edge_arrays()
         assert np.array_equal(deu.cpu().numpy(), eu) and np.array_equal(dev.cpu().numpy(), ev)
         assert s.depth() == oracle.critical_path(len(h), eu, ev)
+
+
+def test_plane_ring_depth_matches_relaxation(cuda):
+    """The shared-memory plane-ring DP (periodic cell-grouped streams) gives the
+    same per-task levels as edge relaxation, incl. plane 0 parked and restored
+    (>= 5 planes), 2D grids and orders with the intra task inside."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    for ext in ((6, 4, 8), (5, 3, 7), (3, 3, 3), (4, 4, 5), (7, 9), (3, 11), (8, 6, 12)):
+        base = P.canonical_half_stencil(len(ext)).offsets
+        inter = list(base[1:])
+        rng.shuffle(inter)
+        k = int(rng.integers(0, len(inter) + 1))
+        order = P.StencilOrder(tuple(inter[:k]) + (base[0],) + tuple(inter[k:]))
+        g = P.GridSpec(ext)
+        s = schedule.device_stream(g, "basic", order)
+        lc, dc = s.levels("chain")
+        lr, dr = s.levels("relax")
+        assert dc == dr, ext
+        assert torch.equal(lc, lr), ext

@@ -6,7 +6,7 @@ from paper_1401_4441_b200 import md
 
 sched = sys.argv[1] if len(sys.argv) > 1 else "shell"
 nuc = int(sys.argv[2]) if len(sys.argv) > 2 else 48
-s = md.LJSystem.fcc(nuc, schedule=sched)
+s = md.LJSystem.fcc(nuc, schedule=sched, skin=0.35)  # (the bench skin)
 for _ in range(3):
     for k in ("fx", "fy", "fz"):
         s._a(k).zero_()
