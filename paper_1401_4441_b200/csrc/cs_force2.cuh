@@ -65,6 +65,7 @@ struct ShellBase {
   int pend[QN];                    // Verlet: contributing homes still running per footprint cell
   int queue[QN];                   // Verlet: footprint cells ready to merge, in order (-1: not yet)
   int qtail, qhead;
+  int rtot, htot;                  // reaction slots / home rows in use (zeroed per block)
   int overflow;
   uint8_t mt_n[SH_MAXF];           // merge-table counts in shared memory (lanes of one warp
                                    //   read different cells: divergent constant reads serialise)
@@ -550,6 +551,8 @@ __device__ __forceinline__ void shell_tables(const ShellArgs &SA, SM &S, const i
     }
     if (lane == 0) {
       S.fstart[0] = 0;
+      S.rtot = min(rb, RCAP);
+      S.htot = min(fb, HCAP);
       S.overflow = (fb > HCAP || rb > RCAP || (!VERLET && src_max > SH_JCAP)) ? 1 : 0;
     }
   }
@@ -628,7 +631,13 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * k), "l"(src + 16 * k)
                      : "memory");
       asm volatile("cp.async.commit_group;" ::: "memory");
-      for (int i = threadIdx.x; i < RCAP + HCAP; i += blockDim.x) S.RF[0][i] = S.RF[1][i] = S.RF[2][i] = 0.0;
+      // zero the slots in use (counts read from the global copy of the tables)
+      const ShellSmemVL &G = *reinterpret_cast<const ShellSmemVL *>(src - offsetof(ShellSmemVL, sh));
+      const int rt = __ldg(&G.rtot), ht = __ldg(&G.htot);
+      for (int i = threadIdx.x; i < rt + ht; i += blockDim.x) {
+        const int k = i < rt ? i : RCAP + i - rt;
+        S.RF[0][k] = S.RF[1][k] = S.RF[2][k] = 0.0;
+      }
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       cached = true;
@@ -669,7 +678,10 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   }
   if (VERLET) vl_pre_positions(A, pre);
   if (!cached)
-    for (int i = threadIdx.x; i < RCAP + HCAP; i += blockDim.x) S.RF[0][i] = S.RF[1][i] = S.RF[2][i] = 0.0;
+    for (int i = threadIdx.x; i < S.rtot + S.htot; i += blockDim.x) {
+      const int k = i < S.rtot ? i : RCAP + i - S.rtot;
+      S.RF[0][k] = S.RF[1][k] = S.RF[2][k] = 0.0;
+    }
   __syncthreads();
 
   const double rc2 = A.p.rc2, sig2 = A.p.sig2, eps48 = A.p.eps48, eps4 = A.p.eps4;
@@ -973,26 +985,34 @@ __global__ void k_block_sizes(ShellArgs SA, int32_t *sizes) {
 
 // buffered mode, pass 2: every particle sums the <= 8 block buffers whose
 // footprint box contains its cell, in a fixed block order (deterministic).
-// One warp per cell: lanes 0..7 resolve the 2x2x2 candidate blocks once.
+// One warp per GB_CELLS consecutive cells: lane (c, k) resolves candidate
+// block k of cell c once, then the warp's lanes walk the cells' particles
+// together (small cells -- a cfg5 vapour cell holds ~0.5 particles -- do not
+// idle a warp each).
+#define GB_CELLS 4
+static_assert(GB_CELLS == 4, "the cell selects below are written out for 4 cells");
 __global__ void k_gather_blocks(ShellArgs SA) {
   const ForceArgs &A = SA.A;
   const Box &b = A.b;
   const int B0 = b.blk[0], B1 = b.blk[1], B2 = b.blk[2];
   const int FX = B0 + 1, FY = B1 + 2, FZ = B2 + 2;
   const int nc0 = b.nc[0], nc1 = b.nc[1];
-  const int ncell = nc0 * nc1 * b.nc[2];
-  const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int64_t ncell = (int64_t)nc0 * nc1 * b.nc[2];
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= ncell) return;
-  const int c0 = warp % nc0, c1 = (warp / nc0) % nc1, c2 = warp / (nc0 * nc1);
-  const int64_t gc = box_cell(b, c0, c1, c2);
-  const int g0 = A.start[gc], n = A.start[gc + 1] - g0;
-  if (n == 0) return;
-  // per axis: the block containing c and, at a block edge, the neighbour
-  // block whose footprint reaches c (x: footprint reaches +1; y, z: -1, +B)
-  int src = -1;
-  if (lane < 8) {
-    const int u = lane & 1, v = (lane >> 1) & 1, w = lane >> 2;
+  const int64_t cfirst = warp * GB_CELLS;
+  if (cfirst >= ncell) return;
+  const int cs = lane >> 3, kk = lane & 7;  // (cell of the group, candidate block)
+  const int64_t cl = cfirst + cs;
+  int src = -1, g0 = 0, n = 0;
+  if (cl < ncell) {
+    const int c0 = (int)(cl % nc0), c1 = (int)((cl / nc0) % nc1), c2 = (int)(cl / ((int64_t)nc0 * nc1));
+    const int64_t gc = box_cell(b, c0, c1, c2);
+    g0 = A.start[gc];
+    n = A.start[gc + 1] - g0;
+    // per axis: the block containing c and, at a block edge, the neighbour
+    // block whose footprint reaches c (x: footprint reaches +1; y, z: -1, +B)
+    const int u = kk & 1, v = (kk >> 1) & 1, w = kk >> 2;
     int k0 = c0 / B0, k1 = c1 / B1, k2 = c2 / B2;
     bool ok = true;
     if (u) { if (c0 % B0 == 0) k0 -= 1; else ok = false; }
@@ -1012,36 +1032,50 @@ __global__ void k_gather_blocks(ShellArgs SA) {
       }
     }
   }
-  // the <= 8 source offsets, then all loads issued before the fixed-order sums
-  int so[8];
+  // particle ranges of the group's cells (lane 8c holds cell c's)
+  int pre[GB_CELLS + 1], gs[GB_CELLS];
+  pre[0] = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) so[k] = __shfl_sync(CS_FULL, src, k);
-  for (int i = lane; i < ((n + 31) & ~31); i += 32) {
+  for (int c = 0; c < GB_CELLS; ++c) {
+    pre[c + 1] = pre[c] + __shfl_sync(CS_FULL, n, 8 * c);
+    gs[c] = __shfl_sync(CS_FULL, g0, 8 * c);
+  }
+  const int ptot = pre[GB_CELLS];
+  for (int t0 = 0; t0 < ptot; t0 += 32) {
+    const int t = t0 + lane;
+    int c = 0;
+#pragma unroll
+    for (int q = 1; q < GB_CELLS; ++q) c += t >= pre[q];
+    const int i = t - (c == 0 ? pre[0] : (c == 1 ? pre[1] : (c == 2 ? pre[2] : pre[3])));
+    const int gi = (c == 0 ? gs[0] : (c == 1 ? gs[1] : (c == 2 ? gs[2] : gs[3]))) + i;
+    // the <= 8 source offsets of this particle's cell, then all loads issued
+    // before the fixed-order sums
     double vx[8], vy[8], vz[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const bool ok = so[k] >= 0 && i < n;
-      const int64_t o = ok ? (int64_t)so[k] + i : 0;
+      const int so = __shfl_sync(CS_FULL, src, 8 * c + k);
+      const bool ok = so >= 0 && t < ptot;
+      const int64_t o = ok ? (int64_t)so + i : 0;
       vx[k] = ok ? __ldcs(SA.buf + o) : 0.0;
       vy[k] = ok ? __ldcs(SA.buf + SA.bufstride + o) : 0.0;
       vz[k] = ok ? __ldcs(SA.buf + 2 * SA.bufstride + o) : 0.0;
     }
     double sx = 0, sy = 0, sz = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {  // same order as before: source lanes ascending
+    for (int k = 0; k < 8; ++k) {  // fixed order: candidate blocks ascending
       sx += vx[k];
       sy += vy[k];
       sz += vz[k];
     }
-    if (i < n) {
+    if (t < ptot) {
       if (SA.overwrite) {
-        A.fx[g0 + i] = sx;
-        A.fy[g0 + i] = sy;
-        A.fz[g0 + i] = sz;
+        A.fx[gi] = sx;
+        A.fy[gi] = sy;
+        A.fz[gi] = sz;
       } else {
-        A.fx[g0 + i] += sx;
-        A.fy[g0 + i] += sy;
-        A.fz[g0 + i] += sz;
+        A.fx[gi] += sx;
+        A.fy[gi] += sy;
+        A.fz[gi] += sz;
       }
     }
   }
@@ -1162,7 +1196,8 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, int mode, bool v
     }
     kern<<<(unsigned)nblocks, SH_NW * 32, smem, st>>>(SA, -1);
     const int64_t ncell = (int64_t)A.b.nc[0] * A.b.nc[1] * A.b.nc[2];
-    k_gather_blocks<<<(unsigned)((ncell * 32 + 255) / 256), 256, 0, st>>>(SA);
+    const int64_t gwarps = (ncell + GB_CELLS - 1) / GB_CELLS;
+    k_gather_blocks<<<(unsigned)((gwarps * 32 + 255) / 256), 256, 0, st>>>(SA);
     return cs_check_launch("force_buffered");
   }
   for (int colour = 0; colour < 8; ++colour) {

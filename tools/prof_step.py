@@ -7,7 +7,11 @@ import torch
 from paper_1401_4441_b200 import md
 
 nsteps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-s = md.LJSystem.fcc(48, schedule="verlet", skin=0.35)
+config = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
+if config == "cfg5":
+    s = md.LJSystem.liquid_vapour(schedule="verlet", seed=42, skin=0.35)
+else:
+    s = md.LJSystem.fcc(48, schedule="verlet", skin=0.35)
 for _ in range(nsteps):
     s.step()
 torch.cuda.synchronize()
