@@ -100,6 +100,13 @@ class ClockSampler:
                  "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a while to start: wait for its first sample so
+            # that sampling is live when the timed region begins, then keep
+            # only the samples taken from here on
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.rows.clear()
         except OSError:
             self.proc = None
         return self
@@ -110,6 +117,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            t0 = time.time()  # a short timed region: take the next sample as well
+            while len(self.rows) < 2 and time.time() - t0 < 0.5 and self.proc.poll() is None:
+                time.sleep(0.005)
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
@@ -495,7 +505,8 @@ def run_ours(args):
                      "achieved_pair_flops": m["achieved_pairs"],
                      "frac_pair_flops": m["achieved_pairs"] / peak_fp64,
                      "peak_source": "measured live: cs_probe_dfma DFMA chains (MEASURED_PEAKS.json has no FP64 entry)",
-                     "hbm_peak_gbs": peaks().get("hbm_gbs")},
+                     "hbm_peak_gbs": peaks().get("hbm_gbs"),
+                     **hbm_side(sysm, statistics.mean(m["force_ms"]), args.schedule)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps * sysm.launches_per_step()
@@ -505,6 +516,25 @@ def run_ours(args):
     if ws == 1 and args.config == "cfg2" and not args.no_schedule:
         line["schedule_analysis"] = schedule_report(torch, cpu=not args.no_cpu)
     print(json.dumps(line), flush=True)
+
+
+def hbm_side(sysm, force_ms, schedule):
+    """The HBM side of the force kernel's roofline: algorithmic bytes per
+    evaluation (48 B/particle: x, y, z in, f out; Verlet adds the round-table
+    descriptors, 64 B per round) and the ncu DRAM traffic, over the measured
+    force-phase time (kernel + buffered gather), against the measured HBM peak."""
+    nbytes = 48 * sysm.n
+    if sysm.verlet:
+        rounds, _ = sysm.list_rounds()
+        nbytes += 64 * int(rounds.sum())
+    hbm = peaks().get("hbm_gbs")
+    out = {"hbm_algorithmic_bytes": nbytes, "hbm_achieved_gbs": nbytes / (force_ms * 1e-3) / 1e9}
+    tr = traffic_bytes(schedule)
+    if tr:
+        out["hbm_traffic_gbs"] = tr / (force_ms * 1e-3) / 1e9
+    if hbm:
+        out["hbm_frac"] = out["hbm_achieved_gbs"] / hbm
+    return out
 
 
 SCHED_GRIDS = {"cfg1": (4, 4, 4), "cfg5": (64, 64, 192)}
