@@ -253,6 +253,15 @@ int cs_lj_forces_verlet(const cs_box *b, const cs_lj *p, int sched, int64_t n,
                         double *energy_dev, unsigned long long *npairs_dev, unsigned *status_dev,
                         void *ws, size_t ws_bytes, void *stream);
 int cs_wrap_positions(int64_t n, const cs_box *b, double *x, double *y, double *z, void *stream);
+/* Post-kick (kick != 0: v += hdtm f) fused with the exact prediction of the next
+ * step's displacement flag (flag[0] = 1 if the next kick-drift, computed from the same
+ * f, would move a particle more than half_skin from x0), so the rebuild decision of
+ * step n+1 is taken at the end of step n (the x-slab step's protocol). */
+int cs_vv_kick_predict(int64_t n, double hdtm, double dt, int kick, const double *fx,
+                       const double *fy, const double *fz, double *vx, double *vy, double *vz,
+                       const double *x, const double *y, const double *z, const double *x0,
+                       const double *y0, const double *z0, double half_skin, int32_t *flag,
+                       void *stream);
 int cs_vv_kick_drift_track(int64_t n, double hdtm, double dt, const double *fx, const double *fy,
                            const double *fz, double *vx, double *vy, double *vz, double *x,
                            double *y, double *z, const double *x0, const double *y0,

@@ -473,6 +473,49 @@ __global__ void k_kick_drift_track(int64_t n, double hdtm, double dt, const doub
   if (__any_sync(CS_FULL, far) && (threadIdx.x & 31) == 0) *flag = 1;  // same value from every writer
 }
 
+// post-kick (kick != 0: v += hdtm f) fused with the exact prediction of the
+// NEXT step's displacement flag: the next kick-drift computes
+// w = fma(hdtm, f, v), x' = fma(dt, w, x) from the same f, so the flag is
+// known at the end of this step (the x-slab step takes its global rebuild
+// decision there, off the critical path of the next step)
+__global__ void k_kick_predict(int64_t n, double hdtm, double dt, int kick, const double *fx,
+                               const double *fy, const double *fz, double *vx, double *vy,
+                               double *vz, const double *x, const double *y, const double *z,
+                               const double *x0, const double *y0, const double *z0, double lim2,
+                               int32_t *flag) {
+  bool far = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double fxi = fx[i], fyi = fy[i], fzi = fz[i];
+    double ux = vx[i], uy = vy[i], uz = vz[i];
+    if (kick) {
+      ux = __fma_rn(hdtm, fxi, ux);
+      uy = __fma_rn(hdtm, fyi, uy);
+      uz = __fma_rn(hdtm, fzi, uz);
+      vx[i] = ux;
+      vy[i] = uy;
+      vz[i] = uz;
+    }
+    const double nx = __fma_rn(dt, __fma_rn(hdtm, fxi, ux), x[i]);
+    const double ny = __fma_rn(dt, __fma_rn(hdtm, fyi, uy), y[i]);
+    const double nz = __fma_rn(dt, __fma_rn(hdtm, fzi, uz), z[i]);
+    const double dx = nx - x0[i], dy = ny - y0[i], dz = nz - z0[i];
+    far |= __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx)) > lim2;
+  }
+  if (__any_sync(CS_FULL, far) && (threadIdx.x & 31) == 0) *flag = 1;  // same value from every writer
+}
+
+extern "C" int cs_vv_kick_predict(int64_t n, double hdtm, double dt, int kick, const double *fx,
+                                  const double *fy, const double *fz, double *vx, double *vy,
+                                  double *vz, const double *x, const double *y, const double *z,
+                                  const double *x0, const double *y0, const double *z0,
+                                  double half_skin, int32_t *flag, void *stream) {
+  if (n <= 0) return CS_OK;
+  k_kick_predict<<<grid_for(n, 256), 256, 0, cs_stream(stream)>>>(
+      n, hdtm, dt, kick, fx, fy, fz, vx, vy, vz, x, y, z, x0, y0, z0, half_skin * half_skin, flag);
+  return cs_check_launch("vv_kick_predict");
+}
+
 extern "C" int cs_wrap_positions(int64_t n, const cs_box *b, double *x, double *y, double *z,
                                  void *stream) {
   if (n <= 0) return CS_OK;

@@ -219,19 +219,34 @@ class SlabStep:
     def start(self, energy=True):
         self._rebuild()
         pe, npairs = self.forces(energy, rebuild=True)
+        if self.verlet:
+            self._decide(kick=False)
         return self._energies(pe, npairs, energy)
+
+    def _decide(self, kick: bool):
+        """Verlet: the post-kick fused with the exact prediction of the next
+        kick-drift's displacement flag, and the global rebuild decision for
+        the next step (one all-reduce) -- taken at the end of this step, so
+        the next one starts without waiting for its own flag."""
+        self.e.kick_predict(kick)
+        self._next_rebuild = self.x.allreduce_max_int(self.e.take_flag()) > 0
 
     def step(self, energy: bool = False, reduce: bool = True):
         """One VV step.  reduce=False (non-energy steps) skips the global sums:
         pair counts stay in the engine's device accumulator (pairs_total)."""
-        self.e.kick_drift()
-        rebuild = True
         if self.verlet:
-            rebuild = self.x.allreduce_max_int(self.e.take_flag()) > 0
+            self.e.kick_drift(track=False)
+            rebuild = self._next_rebuild
+        else:
+            self.e.kick_drift()
+            rebuild = True
         if rebuild:
             self._rebuild()
         pe, npairs = self.forces(energy, rebuild=rebuild)
-        self.e.kick()
+        if self.verlet:
+            self._decide(kick=True)
+        else:
+            self.e.kick()
         if not reduce and not energy:
             return None
         return self._energies(pe, npairs, energy)
@@ -320,6 +335,7 @@ class CudaSlabEngine:
             self.vlist = torch.zeros(int(L.cs_verlet_list_bytes(C.byref(self.cbox))), dtype=torch.uint8, device=d)
             self.xref = [torch.zeros(cap, dtype=f64, device=d) for _ in range(3)]
             self.vflag = torch.zeros(1, dtype=torch.int32, device=d)
+            self.vflag_scratch = torch.zeros(1, dtype=torch.int32, device=d)
 
     def _s(self):
         return _lib.stream_handle()
@@ -347,14 +363,17 @@ class CudaSlabEngine:
         self.n_owned = m
 
     # -- protocol hooks --------------------------------------------------------
-    def kick_drift(self):
+    def kick_drift(self, track: bool = True):
+        """track=False (Verlet, the decision came from kick_predict): the
+        flag goes to a scratch word and is never read."""
         a = self.A
         hdtm = 0.5 * self.dt / self.params.mass
         if self.verlet:  # no wrap between rebuilds; flag particles past skin/2
+            flag = self.vflag if track else self.vflag_scratch
             _lib.call("cs_vv_kick_drift_track", self.n_owned, hdtm, self.dt, _lib.ptr(a["fx"]),
                       _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), _lib.ptr(a["vx"]), _lib.ptr(a["vy"]),
                       _lib.ptr(a["vz"]), _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]),
-                      *(_lib.ptr(t) for t in self.xref), 0.5 * self.skin, _lib.ptr(self.vflag), self._s())
+                      *(_lib.ptr(t) for t in self.xref), 0.5 * self.skin, _lib.ptr(flag), self._s())
             return
         _lib.call("cs_vv_kick_drift", self.n_owned, hdtm, self.dt, C.byref(self.cbox),
                   _lib.ptr(a["fx"]), _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), _lib.ptr(a["vx"]),
@@ -379,6 +398,15 @@ class CudaSlabEngine:
                   _lib.ptr(self.cell_start), _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]),
                   _lib.ptr(self.vlist), self.vlist.numel(), *(_lib.ptr(t) for t in self.xref),
                   self.n_owned, _lib.ptr(self.status), self._s())
+
+    def kick_predict(self, kick: bool = True):
+        """Verlet: post-kick (optional) + this rank's flag for the next step."""
+        a = self.A
+        hdtm = 0.5 * self.dt / self.params.mass
+        _lib.call("cs_vv_kick_predict", self.n_owned, hdtm, self.dt, int(kick), _lib.ptr(a["fx"]),
+                  _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), _lib.ptr(a["vx"]), _lib.ptr(a["vy"]),
+                  _lib.ptr(a["vz"]), _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]),
+                  *(_lib.ptr(t) for t in self.xref), 0.5 * self.skin, _lib.ptr(self.vflag), self._s())
 
     def kick(self):
         a = self.A

@@ -157,11 +157,22 @@ class CpuVerletSlabEngine(CpuSlabEngine):
         self.skin = skin
         self.flag = 0
 
-    def kick_drift(self):
+    def kick_drift(self, track=True):
         self.v = self.v + 0.5 * self.dt * self.f
         self.x = self.x + self.dt * self.v
         d = ((self.x - self.x0) ** 2).sum(1)
-        self.flag = int((d > (0.5 * self.skin) ** 2).any())
+        flag = int((d > (0.5 * self.skin) ** 2).any())
+        if track:
+            self.flag = flag
+        else:  # the step's decision was predicted at the end of the last step
+            assert flag == self.predicted, "predicted rebuild flag differs from the kick-drift flag"
+
+    def kick_predict(self, kick=True):
+        if kick:
+            self.kick()
+        xn = self.x + self.dt * (self.v + 0.5 * self.dt * self.f)  # the next kick-drift
+        d = ((xn - self.x0) ** 2).sum(1)
+        self.flag = self.predicted = int((d > (0.5 * self.skin) ** 2).any())
 
     def take_flag(self):
         f, self.flag = self.flag, 0

@@ -1,5 +1,5 @@
 import sys, time
-sys.path.insert(0, '/root/repo')
+import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1401_4441_b200 import md, slab
 box, nucs, a = md.fcc_box((48, 48, 48), 0.8442)
