@@ -585,7 +585,53 @@ def schedule_report(torch, cpu=True):
         out[cname] = {"grid": list(ext), "orders": rows}
     out["note"] = ("device: stream generation + edge detection + critical path (wall clock incl. "
                    "allocations); cpu_port: oracle/cs_oracle.c restatement of the same pipeline, 1 core")
+    out["payload"] = payload_report(torch, cpu)
     return out
+
+
+def payload_report(torch, cpu=True, ext=(64, 64, 192), seed=42):
+    """The reference's own hot loop, the integer payload (apply_tasks /
+    reference_oracle, payload.py:84-174), on the cfg5 grid: the colour-order
+    stream executed on the device level by level and as the LJ kernel's 27
+    colour passes, and the direct full-neighbourhood sum; the oracle's C port
+    of apply_tasks / reference_oracle on one host core; bit-exact check."""
+    import numpy as np
+
+    from paper_1401_4441_b200 import GridSpec, payload, schedule
+
+    g = GridSpec(ext)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        return r, 1e3 * (time.perf_counter() - t0)
+
+    ds = schedule.device_stream(g, "loopex")
+    ds.levels()
+    acc_lv, t_lv = timed(lambda: payload.apply_stream_device(ds, seed))
+    acc_cp, t_cp = timed(lambda: payload.colour_pass_payload(g, seed, "loopex", race_check=False))
+    acc_dir, t_dir = timed(lambda: payload.reference_oracle_device(g, seed))
+    row = {"grid": list(ext), "tasks": ds.ntasks, "device_levels_ms": t_lv, "device_colour_passes_ms": t_cp,
+           "device_direct_ms": t_dir,
+           "device_equal": bool(torch.equal(acc_lv, acc_cp) and torch.equal(acc_lv, acc_dir))}
+    if cpu:
+        from oracle import oracle as O
+
+        h, nb, e = ds.home.cpu().numpy(), ds.nbr.cpu().numpy(), ds.entry.cpu().numpy()
+        t0 = time.perf_counter()
+        ref = O.payload_apply(ext, (1, 1, 1), seed, h, nb, e, np.array(ds.entries, np.int8))
+        row["cpu_port_apply_tasks_ms"] = 1e3 * (time.perf_counter() - t0)
+        t0 = time.perf_counter()
+        ref2 = O.payload_reference(ext, (1, 1, 1), seed)
+        row["cpu_port_reference_oracle_ms"] = 1e3 * (time.perf_counter() - t0)
+        row["bit_exact_vs_cpu_port"] = bool(np.array_equal(acc_lv.cpu().numpy(), ref)
+                                            and np.array_equal(ref, ref2))
+    row["note"] = ("reference Python apply_tasks: 10-14 us/task standalone (SURVEY 8a a14, survey "
+                   "container), i.e. about 2 min for these tasks")
+    return row
 
 
 def e2e_run(torch, md, ref_sys, args):
