@@ -238,7 +238,9 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded FCC + jitter, Gaussian velocities)",
-        "config": {"workload": workload_of(args.config),
+        "config": {"workload": workload_of(args.config) + (
+                       f"; the GPU arm at N={ws} runs {ws} such blocks (x-slab weak scaling), the CPU rate "
+                       f"is per pair, sampled on one block" if ws > 1 else ""),
                    "schedule": "loop-exchange colour order, 27 levels, OpenMP over tasks of a level",
                    "steps_per_s": args.steps / tot},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
