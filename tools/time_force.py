@@ -17,12 +17,12 @@ else:
     s = md.LJSystem.fcc(48, schedule=sched, skin=0.35)
 st = torch.cuda.current_stream()
 for _ in range(5):
-    s.compute_forces(energy=False, count_pairs=False)
+    s.compute_forces(energy=False, count_pairs=True)
 torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
 for k in range(reps):
     ev[k].record()
-    s.compute_forces(energy=False, count_pairs=False)
+    s.compute_forces(energy=False, count_pairs=True)
 ev[reps].record()
 torch.cuda.synchronize()
 t = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(reps))
