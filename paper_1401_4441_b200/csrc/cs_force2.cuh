@@ -65,6 +65,7 @@ struct ShellBase {
   int pend[QN];                    // Verlet: contributing homes still running per footprint cell
   int queue[QN];                   // Verlet: footprint cells ready to merge, in order (-1: not yet)
   int qtail, qhead;
+  int nq;                          // Verlet: non-empty footprint cells (merge-queue length)
   int rtot, htot;                  // reaction slots / home rows in use (zeroed per block)
   int overflow;
   uint8_t mt_n[SH_MAXF];           // merge-table counts in shared memory (lanes of one warp
@@ -345,11 +346,13 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
     const bool shift = __any_sync(CS_FULL, lane < 14 && (S.sh[h][lane < 14 ? lane : 0][0] != 0.0 ||
                                                          S.sh[h][lane < 14 ? lane : 0][1] != 0.0 ||
                                                          S.sh[h][lane < 14 ? lane : 0][2] != 0.0));
-    if (shift)
-      verlet_table<ENERGY, true>(S, A, h, v, dp, fa, fb, pe, hits);
-    else
-      verlet_table<ENERGY, false>(S, A, h, v, dp, fa, fb, pe, hits);
-    verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2], pB, fb[0], fb[1], fb[2]);
+    if (v.nr > 0) {  // (a home without listed pairs adds nothing)
+      if (shift)
+        verlet_table<ENERGY, true>(S, A, h, v, dp, fa, fb, pe, hits);
+      else
+        verlet_table<ENERGY, false>(S, A, h, v, dp, fa, fb, pe, hits);
+      verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2], pB, fb[0], fb[1], fb[2]);
+    }
     // this home's slots are final: count it off its 14 footprint cells; the
     // last contributor of a cell queues it for merging
     asm volatile("fence.acq_rel.cta;" ::: "memory");
@@ -360,6 +363,7 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
         atomicExch(&S.queue[q], lc);
       }
     }
+    if (v.nr == 0) return;
     hits = warp_sum(hits);
     if (ENERGY) pe = warp_sum(pe);
     if (lane == 0) {
@@ -570,18 +574,22 @@ __device__ __forceinline__ void shell_tables(const ShellArgs &SA, SM &S, const i
       if (lc < nfc) S.mt_base[lc][k] = (int16_t)base;
       live += base >= 0;
     }
-    if (VERLET) {
-      S.pend[lc] = live;
+    if (VERLET) {  // empty footprint cells have nothing to merge: never queued
+      const bool empty = lc < nfc && (S.fgstart[lc] < 0 || S.fstart[lc + 1] == S.fstart[lc]);
+      S.pend[lc] = empty ? (1 << 20) : live;
       S.queue[lc] = -1;
     }
   }
   __syncthreads();
   if (VERLET && threadIdx.x == 0) {  // cells nobody writes are ready from the start
-    int n0 = 0;
-    for (int lc = 0; lc < nfc; ++lc)
+    int n0 = 0, nq = 0;
+    for (int lc = 0; lc < nfc; ++lc) {
       if (S.pend[lc] == 0) S.queue[n0++] = lc;
+      nq += S.pend[lc] < (1 << 20);
+    }
     S.qtail = n0;
     S.qhead = 0;
+    S.nq = nq;
   }
   __syncthreads();
 }
@@ -835,7 +843,7 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   }
   }  // link-cell super-tasks
   if constexpr (VERLET) {
-    verlet_merge_queue<MODE>(SA, S, lane, nfc, BUFFERED ? SA.boff[bid] : 0);
+    verlet_merge_queue<MODE>(SA, S, lane, S.nq, BUFFERED ? SA.boff[bid] : 0);
     if (BUFFERED)
       for (int lc = threadIdx.x; lc <= nfc; lc += blockDim.x)
         SA.bindex[(int64_t)bid * (SH_MAXF + 1) + lc] = S.fstart[lc];
