@@ -337,7 +337,7 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
                                               const VPre &v) {
   {
     const int h = wid, cell = v.cell;
-    if (cell < 0) return;
+    if (cell < 0 || v.nr == 0) return;  // (not a contributor of any footprint cell)
     const int pA = v.pA, pB = v.pB;
     double pe = 0;
     unsigned hits = 0;
@@ -346,13 +346,11 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
     const bool shift = __any_sync(CS_FULL, lane < 14 && (S.sh[h][lane < 14 ? lane : 0][0] != 0.0 ||
                                                          S.sh[h][lane < 14 ? lane : 0][1] != 0.0 ||
                                                          S.sh[h][lane < 14 ? lane : 0][2] != 0.0));
-    if (v.nr > 0) {  // (a home without listed pairs adds nothing)
-      if (shift)
-        verlet_table<ENERGY, true>(S, A, h, v, dp, fa, fb, pe, hits);
-      else
-        verlet_table<ENERGY, false>(S, A, h, v, dp, fa, fb, pe, hits);
-      verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2], pB, fb[0], fb[1], fb[2]);
-    }
+    if (shift)
+      verlet_table<ENERGY, true>(S, A, h, v, dp, fa, fb, pe, hits);
+    else
+      verlet_table<ENERGY, false>(S, A, h, v, dp, fa, fb, pe, hits);
+    verlet_fi(S, h, lane, pA, fa[0], fa[1], fa[2], pB, fb[0], fb[1], fb[2]);
     // this home's slots are final: count it off its 14 footprint cells; the
     // last contributor of a cell queues it for merging
     asm volatile("fence.acq_rel.cta;" ::: "memory");
@@ -363,7 +361,6 @@ __device__ __forceinline__ void verlet_rounds(SM &S, const ForceArgs &A, int lan
         atomicExch(&S.queue[q], lc);
       }
     }
-    if (v.nr == 0) return;
     hits = warp_sum(hits);
     if (ENERGY) pe = warp_sum(pe);
     if (lane == 0) {
@@ -569,7 +566,9 @@ __device__ __forceinline__ void shell_tables(const ShellArgs &SA, SM &S, const i
       if (lc < nfc && k < SA.mt.n[lc]) {
         const int he = SA.mt.he[lc][k];
         const int hh = he >> 4, e = he & 15;
-        if (S.hcell[hh] >= 0) base = S.sbase[hh][e];
+        // (Verlet: a home without listed pairs adds nothing, so it is not a
+        // contributor -- its warp skips the pend countdown, see verlet_rounds)
+        if (S.hcell[hh] >= 0 && (!VERLET || A.vl_nround[S.hcell[hh]] > 0)) base = S.sbase[hh][e];
       }
       if (lc < nfc) S.mt_base[lc][k] = (int16_t)base;
       live += base >= 0;

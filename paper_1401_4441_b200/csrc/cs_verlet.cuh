@@ -571,6 +571,7 @@ extern "C" int cs_verlet_build(const cs_box *bx, const cs_lj *lj, double skin,
     memset(&SA, 0, sizeof(SA));
     SA.A.b = b;
     SA.A.start = cell_start;
+    SA.A.vl_nround = L.nround;  // (a home without listed pairs is not a merge contributor)
     for (int k = 0; k < 3; ++k) SA.A.nbk[k] = nbk[k];
     const int B[3] = {b.blk[0], b.blk[1], b.blk[2]};
     if (b.blk[0] * b.blk[1] * b.blk[2] <= SH_MAXB && build_merge_table(B, &SA.mt) == CS_OK) {
