@@ -131,17 +131,16 @@ __device__ __forceinline__ bool verlet_pair(SM &S, const ForceArgs &A, int h, un
   double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
   if (!SHIFT && e == 15) r2 = 1e300;
   const bool hit = r2 < A.p.rc2;
-  fx = fy = fz = 0.0;
-  if (hit) {
-    const double ri = fast_rcp(r2);
-    const double s2 = A.p.sig2 * ri;
-    const double s6 = s2 * s2 * s2;
-    const double ff = A.p.eps48 * s6 * (s6 - 0.5) * ri;
-    fx = ff * dx;
-    fy = ff * dy;
-    fz = ff * dz;
-    if (ENERGY) pe += A.p.eps4 * s6 * (s6 - 1.0);
-  }
+  // evaluated for every listed pair (misses select a zero force), so the two
+  // pairs of a round pair form one basic block and their chains interleave
+  const double ri = fast_rcp(hit ? r2 : 1.0);
+  const double s2 = A.p.sig2 * ri;
+  const double s6 = s2 * s2 * s2;
+  const double ff = hit ? A.p.eps48 * s6 * (s6 - 0.5) * ri : 0.0;
+  fx = ff * dx;
+  fy = ff * dy;
+  fz = ff * dz;
+  if (ENERGY) pe += hit ? A.p.eps4 * s6 * (s6 - 1.0) : 0.0;
   return hit;
 }
 
