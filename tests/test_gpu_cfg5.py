@@ -26,7 +26,7 @@ def by_id(snap, key):
     return snap[key][np.argsort(snap["id"])]
 
 
-@pytest.mark.parametrize("sched", ["buffered", "dataflow", "verlet"])
+@pytest.mark.parametrize("sched", ["buffered", "dataflow", "verlet", "verlet_shell", "verlet_dataflow"])
 def test_cfg5_small_forces(oracle, cuda, sched):
     s = md.LJSystem.liquid_vapour(CELLS, schedule=sched, skin=0.3)
     snap = s.snapshot()
