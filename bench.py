@@ -64,6 +64,17 @@ def workload_of(config):
     return WORKLOAD.replace("cfg2: LJ fluid FCC 48^3 = 442368", f"{config}: LJ fluid FCC {k}^3 = {4 * k ** 3}")
 
 
+def ncu_fp64_pipe(schedule):
+    """FP64 pipe activity (% of peak, ncu) of the schedule's force kernel, from
+    the committed capture (profiles/r01_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            t = json.load(f)
+        return t["kernels"]["verlet" if schedule.startswith("verlet") else "buffered"].get("fp64_pipe_active_pct")
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def traffic_bytes(schedule):
     """DRAM bytes per force launch of the schedule's kernel, from the committed
     ncu --set full capture (profiles/r01_traffic.json)."""
@@ -508,6 +519,7 @@ def run_ours(args):
                      "frac_pair_flops": m["achieved_pairs"] / peak_fp64,
                      "peak_source": "measured live: cs_probe_dfma DFMA chains (MEASURED_PEAKS.json has no FP64 entry)",
                      "hbm_peak_gbs": peaks().get("hbm_gbs"),
+                     "ncu_fp64_pipe_active_pct": ncu_fp64_pipe(args.schedule),
                      **hbm_side(sysm, statistics.mean(m["force_ms"]), args.schedule)},
         "cpu_baseline": cpu,
         "e2e": e2e,
