@@ -225,6 +225,29 @@ def cpu_sample(nthreads, min_seconds=10.0, max_steps=200, config="cfg2"):
             return pairs / el, steps, el
 
 
+def cpu_task_replay(config="cfg2"):
+    """one LJ force evaluation as an apply_tasks-style replay
+    (payload.py:84-119) of the reference's own colour-order stream
+    (generate_loopex, taskgen.py:202-234) on ONE host core -- the oracle's C
+    restatement.  Returns (pairs/s, seconds)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    nuc = FCC_CONFIGS[config]
+    a = (4 / 0.8442) ** (1 / 3)
+    L = nuc * a
+    x, y, z = O.fcc_positions([nuc] * 3, [a] * 3, [L] * 3, 0.05, 42)
+    nc = [int(L // 2.5)] * 3
+    _, start, order = O.bin_cells(x, y, z, np.arange(len(x), dtype=np.int32), nc, [c / L for c in nc])
+    xs, ys, zs = (np.ascontiguousarray(v[order]) for v in (x, y, z))
+    h, nb, e = O.stream_loopex(nc, (1, 1, 1))
+    t0 = time.perf_counter()
+    _, _, npair = O.lj_tasks(nc, [L] * 3, start, xs, ys, zs, h, nb, e, O.canonical_stencil(3))
+    el = time.perf_counter() - t0
+    return npair / el, el
+
+
 def run_reference(args):
     rank, ws = dist_init()
     if rank != 0:
@@ -476,6 +499,12 @@ def run_ours(args):
         v, nst, el = cpu_sample(cores, min_seconds=args.cpu_seconds, config=args.config)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{nst} whole {args.config} VV steps in {el:.1f} s (oracle o_md_steps, loop-exchange colour order on OpenMP threads)"}
+        if args.config in FCC_CONFIGS and args.config != "cfg4":
+            v1, el1 = cpu_task_replay(args.config)
+            cpu["single_core_task_replay"] = {
+                "value": v1, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"one {args.config} force evaluation ({el1:.2f} s): apply_tasks-style replay of the "
+                          "reference's generate_loopex stream (oracle o_lj_tasks)"}
     n = sysm.n
     tot_s = m["tot_s"]
     cfg = {"workload": workload_of(args.config), "particles_per_gpu": n, "schedule": f"{args.schedule} {sysm.block}",
