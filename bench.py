@@ -304,8 +304,10 @@ def fp64_peak(torch, lib):
 
 
 def run_slab(args, rank, ws):
-    """N > 1: x-slab decomposition, each rank owns a cfg2-sized slab (32 of
-    32N cell planes, 442,368 particles per GPU), halos/migration over NCCL."""
+    """N > 1: x-slab decomposition, halos/migration over NCCL.  cfg2 (the
+    default): weak scaling, each rank owns a cfg2-sized slab (28 of 28N
+    Verlet cell planes, 442,368 particles per GPU).  cfg3 / cfg4 / cfg5:
+    strong scaling, the configuration's box cut into N x-slabs."""
     import torch
 
     from paper_1401_4441_b200 import _lib, md, slab
@@ -314,11 +316,18 @@ def run_slab(args, rank, ws):
     verlet = args.schedule in md.VERLET_SCHEDULES
     if verlet:
         args.schedule = "verlet"  # buffered block schedule on the rank-local grid
-    nuc = (NUC * ws, NUC, NUC)
-    box, nucs, a = md.fcc_box(nuc, 0.8442)
-    n = 4 * nucs[0] * nucs[1] * nucs[2]
-    g = md.LJSystem(box, n, schedule="loopex")  # global initial state (same on every rank)
-    g.seed_fcc(nucs, a, 0.722, 0.05, 42)
+    weak = args.config == "cfg2"
+    # global initial state (same on every rank), built by the single-domain system
+    if args.config == "cfg5":
+        g = md.LJSystem.liquid_vapour(schedule="buffered", seed=42)
+        box, n = g.box, g.n
+        nuc = None
+    else:
+        nuc = (NUC * ws, NUC, NUC) if weak else (FCC_CONFIGS[args.config],) * 3
+        box, nucs, a = md.fcc_box(nuc, 0.8442)
+        n = 4 * nucs[0] * nucs[1] * nucs[2]
+        g = md.LJSystem(box, n, schedule="loopex")
+        g.seed_fcc(nucs, a, 0.722, 0.05, 42)
     ini = {k: v[:n] for k, v in g.initial.items()}
     if verlet:  # cells of edge >= rc + skin (y, z multiples of 4 for the block colouring)
         c = md.LJBox.for_cutoff(box.lengths, 2.5 + args.skin).cells
@@ -365,13 +374,17 @@ def run_slab(args, rank, ws):
     clocks = clk.summary()
     if rank != 0:
         return
+    workload = (f"cfg2 per GPU, x-slab weak scaling: FCC {nuc[0]}x48x48 = {n} particles, " if weak else
+                f"{args.config} ({n} particles) cut into {ws} x-slabs (strong scaling): ")
     line = {
-        "metric": METRIC, "value": pairs / tot_s, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": METRIC if weak else metric_of(args.config), "value": pairs / tot_s, "unit": UNIT,
+        "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded FCC + 0.05 sigma jitter, Gaussian velocities)",
-        "config": {"workload": f"cfg2 per GPU, x-slab weak scaling: FCC {nuc[0]}x48x48 = {n} particles, "
-                               f"{box.cells[0]}x{box.cells[1]}x{box.cells[2]} cells, {lay.owned} planes per rank",
+        "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": ("synthetic (seeded liquid slab + rejection-sampled vapour, Gaussian velocities; BASELINE cfg5)"
+                 if args.config == "cfg5" else "synthetic (seeded FCC + 0.05 sigma jitter, Gaussian velocities)"),
+        "config": {"workload": workload + f"{box.cells[0]}x{box.cells[1]}x{box.cells[2]} cells, "
+                               f"{lay.owned} planes per rank",
                    "schedule": f"{args.schedule} (2, 2, 2) on the rank-local grid"
                                + (f", skin {args.skin}, list rebuilds {st.rebuilds} (all ranks together, "
                                   "migration only at rebuilds)" if verlet else ""),
