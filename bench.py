@@ -351,7 +351,9 @@ def run_slab(args, rank, ws):
             torch.cuda.synchronize()
             barrier(ws)
             ev[k][0].record()
-            st.step(energy=False, reduce=False)  # pair counts stay on the device
+            # pair counts stay on the device; each step but the last launches the
+            # next one's kick-drift before waiting for the rebuild decision
+            st.step(energy=False, reduce=False, lookahead=k < args.steps - 1)
             ev[k][1].record()
             torch.cuda.synchronize()
     pairs = st.pairs_total() - p0  # summed over ranks

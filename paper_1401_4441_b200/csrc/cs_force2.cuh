@@ -656,6 +656,9 @@ __device__ __forceinline__ void shell_block(const ShellArgs &SA, unsigned char *
   if (S.overflow) {
     if constexpr (MODE != SH_COLOUR) {  // no in-place fallback: report to the host
       if (threadIdx.x == 0) atomicExch(SA.err, 1u);
+      if (BUFFERED)  // the gather still reads this block's (unwritten) buffer in bounds
+        for (int lc = threadIdx.x; lc <= nfc; lc += blockDim.x)
+          SA.bindex[(int64_t)bid * (SH_MAXF + 1) + lc] = S.fstart[lc];
       return;
     } else {
     // colour mode fallback: v1 per-task routine on global memory under the 27

@@ -176,6 +176,7 @@ class SlabStep:
         # in between, the ghost plane keeps its particles and order
         self.verlet = bool(getattr(engine, "verlet", False))
         self.rebuilds = 0
+        self._kd_ahead = False
 
     def migrate(self):
         stay, to_left, to_right = self.e.split()
@@ -223,19 +224,32 @@ class SlabStep:
             self._decide(kick=False)
         return self._energies(pe, npairs, energy)
 
-    def _decide(self, kick: bool):
+    def _decide(self, kick: bool, lookahead: bool = False):
         """Verlet: the post-kick fused with the exact prediction of the next
         kick-drift's displacement flag, and the global rebuild decision for
         the next step (one all-reduce) -- taken at the end of this step, so
         the next one starts without waiting for its own flag."""
         self.e.kick_predict(kick)
+        if lookahead:
+            self.e.kick_drift(track=False)
+            self._kd_ahead = True
         self._next_rebuild = self.x.allreduce_max_int(self.e.take_flag()) > 0
 
-    def step(self, energy: bool = False, reduce: bool = True):
+    def step(self, energy: bool = False, reduce: bool = True, lookahead: bool = False):
         """One VV step.  reduce=False (non-energy steps) skips the global sums:
-        pair counts stay in the engine's device accumulator (pairs_total)."""
+        pair counts stay in the engine's device accumulator (pairs_total).
+
+        lookahead=True (Verlet, non-energy steps): the NEXT step's kick-drift
+        -- which does not depend on the rebuild decision -- is launched before
+        this step waits for that decision, so the device is not idle while
+        the host takes it.  The state then stands half a step ahead until the
+        next step() call: use it only inside a run of steps (not on the last
+        one, and not when the state is read in between)."""
         if self.verlet:
-            self.e.kick_drift(track=False)
+            if self._kd_ahead:
+                self._kd_ahead = False  # launched by the previous step
+            else:
+                self.e.kick_drift(track=False)
             rebuild = self._next_rebuild
         else:
             self.e.kick_drift()
@@ -244,7 +258,7 @@ class SlabStep:
             self._rebuild()
         pe, npairs = self.forces(energy, rebuild=rebuild)
         if self.verlet:
-            self._decide(kick=True)
+            self._decide(kick=True, lookahead=lookahead and not energy)
         else:
             self.e.kick()
         if not reduce and not energy:

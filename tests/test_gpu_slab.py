@@ -175,3 +175,32 @@ def _run_verlet(world, nuc, steps, skin, oracle, cuda):
 @pytest.mark.parametrize("world", [1, 2, 3])
 def test_slab_verlet(oracle, cuda, world):
     _run_verlet(world, 14, 10, 0.12, oracle, cuda)
+
+
+def test_slab_lookahead_is_bit_identical(cuda):
+    """SlabStep(lookahead=True) launches the next kick-drift before the
+    rebuild decision; over a run with rebuilds the result is bit for bit the
+    plain stepping's."""
+    import torch
+    from paper_1401_4441_b200 import md, slab
+
+    g = md.LJSystem.fcc(14, schedule="verlet", skin=0.12)  # the global initial state (10,976 particles)
+    box, n = g.box, g.n
+    ini = {k: v[:n] for k, v in g.initial.items()}
+    c = md.LJBox.for_cutoff(box.lengths, 2.5 + 0.12).cells  # 8^3 Verlet cells, ~21 particles each
+    vbox = md.LJBox(box.lengths, (c[0] - c[0] % 2,) + tuple(v - v % 4 for v in c[1:]))
+    out = []
+    for la in (False, True):
+        lay = slab.SlabLayout(vbox.cells[0], 1, 0)
+        eng = slab.CudaSlabEngine(vbox, lay, md.LJParams(), schedule="verlet", skin=0.12)
+        eng.load_global(*(ini[k] for k in ("x", "y", "z", "vx", "vy", "vz", "id")))
+        st = slab.SlabStep(eng, slab.NeighbourExchanger(lay))
+        st.start(energy=True)
+        nsteps = 25
+        for k in range(nsteps):
+            st.step(energy=False, reduce=False, lookahead=la and k < nsteps - 1)
+        torch.cuda.synchronize()
+        out.append((st.rebuilds, eng.owned_arrays()))
+    assert out[0][0] == out[1][0] and out[0][0] >= 2
+    for key in ("id", "x", "v", "f"):
+        assert (out[0][1][key] == out[1][1][key]).all(), key

@@ -22,4 +22,4 @@ for _ in range(30): st.step(energy=False, reduce=False)
 pr.disable()
 torch.cuda.synchronize()
 print("host ms/step", (time.perf_counter() - t0) / 30 * 1e3, "rebuilds", st.rebuilds)
-pstats.Stats(pr).sort_stats("cumtime").print_stats(18)
+pstats.Stats(pr).sort_stats("tottime").print_stats(25)
