@@ -112,8 +112,11 @@ __device__ __forceinline__ void vl_source(const Box &b, const int32_t *start, in
 #define VB_NCH (VB_JCAP / 32)  // candidate chunks per home cell
 #define VB_SEG 4                // table lanes a particle may span
 
+// The round table is placed directly in its global slot (no shared copy), which
+// leaves 28.5 KB of shared memory per CTA; at <= 70 registers 7 CTAs (28 warps)
+// fit an SM (measured: rebuild 865 -> 825 us on cfg2).
+#define VB_MINB 7
 struct VBuildSmem {
-  uint16_t tab[VB_NW][VL_RMAX][32];         // round table of the current cell
   unsigned used[VB_NW][2][VB_JCAP];         // per candidate j: rounds taken (low, high 32)
   unsigned row[VB_NW][32][VB_NCH];          // particle -> candidate bits per chunk
   uint16_t code[VB_NW][VB_JCAP];            // entry << 8 | index in the source cell
@@ -230,14 +233,12 @@ __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
   return __all_sync(CS_FULL, ok);
 }
 
-__global__ void __launch_bounds__(VB_NW * 32) k_verlet_build(Box b, const int32_t *start,
+__global__ void __launch_bounds__(VB_NW * 32, VB_MINB) k_verlet_build(Box b, const int32_t *start,
                                                              const double *x, const double *y,
                                                              const double *z, double rl2,
                                                              VList L, unsigned *status) {
   __shared__ VBuildSmem S;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < VB_NW * VL_RMAX * 32; k += blockDim.x) (&S.tab[0][0][0])[k] = VL_IDLE;
-  __syncthreads();
   const int64_t nhome = (int64_t)b.owned_x * b.nc[1] * b.nc[2];
   for (int64_t t = (int64_t)blockIdx.x * VB_NW + w; t < nhome; t += (int64_t)gridDim.x * VB_NW) {
     const int h0 = (int)(t % b.owned_x), h1 = (int)((t / b.owned_x) % b.nc[1]),
@@ -370,6 +371,8 @@ __global__ void __launch_bounds__(VB_NW * 32) k_verlet_build(Box b, const int32_
           lo = 0;
         }
       }
+      uint16_t(*tab)[32] = reinterpret_cast<uint16_t(*)[32]>(L.desc + cell * (VL_RMAX * 32));
+      for (int r = 0; r < R; ++r) tab[r][lane] = VL_IDLE;
       // lane -> (first particle, second particle, switch round)
       S.lmap[w][lane] = S.lmap[w][32 + lane] = 0xFF;
       S.lmap[w][64 + lane] = (uint8_t)R;
@@ -394,17 +397,16 @@ __global__ void __launch_bounds__(VB_NW * 32) k_verlet_build(Box b, const int32_
 #pragma unroll
         for (int k = 0; k < VB_SEG; ++k) f32[k] = (unsigned)fr[k];
         ok = vl_place(S.row[w][lane < na ? lane : 0], lane < na ? nch : 0, f32, seg_l, S.used[w],
-                      S.code[w], S.tab[w], lane);
+                      S.code[w], tab, lane);
       } else {
         ok = vl_place(S.row[w][lane < na ? lane : 0], lane < na ? nch : 0, fr, seg_l, S.used[w],
-                      S.code[w], S.tab[w], lane);
+                      S.code[w], tab, lane);
       }
       if (ok) {
         placed = true;
       } else {  // a pair found no free round: clear and retry with one more round
-        for (int r = 0; r < R; ++r) S.tab[w][r][lane] = VL_IDLE;
         __syncwarp();
-        ++R;
+        ++R;  // (the next attempt re-initialises its rounds)
       }
     }
     if (!placed) {
@@ -419,11 +421,6 @@ __global__ void __launch_bounds__(VB_NW * 32) k_verlet_build(Box b, const int32_
     lm[lane] = S.lmap[w][lane];
     lm[32 + lane] = S.lmap[w][32 + lane];
     lm[64 + lane] = S.lmap[w][64 + lane];
-    uint16_t *dst = L.desc + cell * (VL_RMAX * 32) + lane;
-    for (int r = 0; r < R; ++r) {
-      dst[r * 32] = S.tab[w][r][lane];
-      S.tab[w][r][lane] = VL_IDLE;
-    }
     __syncwarp();
   }
 }
