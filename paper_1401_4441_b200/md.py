@@ -335,9 +335,10 @@ class LJSystem:
         """Copy host arrays in (any order), rebuild cells and forces."""
         torch = _torch()
         b = self._buf[self.cur]
+        # (non-blocking: pinned host sources overlap; pageable ones copy synchronously)
         for k, arr in zip(("x", "y", "z", "vx", "vy", "vz"), (x, y, z, vx, vy, vz)):
-            b[k][: self.n].copy_(torch.as_tensor(arr, dtype=torch.float64))
-        b["id"][: self.n].copy_(torch.as_tensor(ids, dtype=torch.int32))
+            b[k][: self.n].copy_(torch.as_tensor(arr, dtype=torch.float64), non_blocking=True)
+        b["id"][: self.n].copy_(torch.as_tensor(ids, dtype=torch.int32), non_blocking=True)
         self.rebuild()
 
     def rebuild(self, energy: bool = True):
