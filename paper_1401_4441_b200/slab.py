@@ -354,13 +354,17 @@ class CudaSlabEngine:
     def _s(self):
         return _lib.stream_handle()
 
-    def load_global(self, x, y, z, vx, vy, vz, ids):
-        """Take this rank's particles out of global device arrays (same
-        classification kernel as the migration)."""
+    def load_global(self, x, y, z, vx, vy, vz, ids, global_n: int | None = None):
+        """Take this rank's particles out of device arrays holding the global
+        state or any superset of this rank's particles (same classification
+        kernel as the migration; the others are dropped).  global_n: the
+        total particle count when the arrays hold a subset (sizes the
+        buffers)."""
         torch = _torch()
         n = int(x.numel())
-        if self.cap == 0:
-            self._alloc(int(n / self.layout.world * 1.3) + 4 * self.plane_cells * 32 + 4096)
+        if not hasattr(self, "A"):
+            tot = int(global_n) if global_n else n
+            self._alloc(self.cap or int(tot / self.layout.world * 1.3) + 4 * self.plane_cells * 32 + 4096)
         big = torch.zeros(7 * n, dtype=torch.float64, device=self.device)
         scratch = torch.zeros(7 * n, dtype=torch.float64, device=self.device)
         ws = torch.empty(_lib.load().cs_slab_ws_bytes(n), dtype=torch.uint8, device=self.device)
