@@ -237,7 +237,7 @@ int cs_lj_forces(const cs_box *b, const cs_lj *p, int sched, int64_t n,
  * colour-pass / buffered block structure of K2 is unchanged.
  * cs_verlet_build: list from the current (wrapped, binned) positions, and
  *   x0/y0/z0 = copy of x/y/z (reference for the displacement check, may be
- *   NULL).  status_dev |= 2 (a cell holds > 32 particles) or 4 (> 64 rounds).
+ *   NULL).  status_dev |= 2 (a cell holds > 64 particles) or 4 (> 64 rounds).
  * cs_lj_forces_verlet: sched CS_SCHED_SHELL or CS_SCHED_BUFFERED; overwrites f.
  * Between rebuilds positions must NOT be wrapped: cs_vv_kick_drift_track is
  *   kick_drift without the wrap, setting flag[0] = 1 once a particle is more

@@ -37,6 +37,8 @@ struct VList {
   int32_t *boff;    //   their exclusive scan = block buffer offsets
   void *scan_ws;    //   scan scratch
   unsigned char *tab;  // per-block force-kernel tables (vl_table_bytes each)
+  int32_t *crowd;      // builder: home cells above 32 particles (second pass)
+  int32_t *ncrowd;     //   and their count
 };
 
 static int64_t vl_blocks(const Box &b) {
@@ -49,10 +51,12 @@ static size_t vl_bytes(const Box &b) {  // (blocks <= cells bounds the layout ar
   return cs_ws_slice(sizeof(int32_t) * ncell) + cs_ws_slice(96 * (size_t)ncell) +
          cs_ws_slice(sizeof(uint16_t) * (size_t)VL_RMAX * 32 * ncell) +
          2 * cs_ws_slice(sizeof(int32_t) * (ncell + 2)) + cs_ws_slice(cs_scan_ws_bytes(ncell + 1)) +
-         cs_ws_slice(vl_table_bytes() * (size_t)vl_blocks(b));
+         cs_ws_slice(vl_table_bytes() * (size_t)vl_blocks(b)) + cs_ws_slice(sizeof(int32_t) * ncell) +
+         cs_ws_slice(64);
 }
 
-static VList vl_view(void *p, int64_t ncell) {
+static VList vl_view(void *p, const Box &b) {
+  const int64_t ncell = b.ncells;
   char *c = (char *)p;
   VList v;
   v.nround = (int32_t *)c;
@@ -68,11 +72,15 @@ static VList vl_view(void *p, int64_t ncell) {
   v.scan_ws = c;
   c += cs_ws_slice(cs_scan_ws_bytes(ncell + 1));
   v.tab = (unsigned char *)c;
+  c += cs_ws_slice(vl_table_bytes() * (size_t)vl_blocks(b));
+  v.crowd = (int32_t *)c;
+  c += cs_ws_slice(sizeof(int32_t) * ncell);
+  v.ncrowd = (int32_t *)c;
   return v;
 }
 
 static void vl_attach(ForceArgs &A, const void *vlist) {
-  VList v = vl_view(const_cast<void *>(vlist), A.b.ncells);
+  VList v = vl_view(const_cast<void *>(vlist), A.b);
   A.vl_nround = v.nround;
   A.vl_imap = v.imap;
   A.vl_desc = v.desc;
@@ -109,20 +117,27 @@ __device__ __forceinline__ void vl_source(const Box &b, const int32_t *start, in
   }
 }
 
-#define VB_NCH (VB_JCAP / 32)  // candidate chunks per home cell
 #define VB_SEG 4                // table lanes a particle may span
 
-// The round table is placed directly in its global slot (no shared copy), which
-// leaves 28.5 KB of shared memory per CTA; at <= 70 registers 7 CTAs (28 warps)
-// fit an SM (measured: rebuild 865 -> 825 us on cfg2).
-#define VB_MINB 7
-struct VBuildSmem {
-  unsigned used[VB_NW][2][VB_JCAP];         // per candidate j: rounds taken (low, high 32)
-  unsigned row[VB_NW][32][VB_NCH];          // particle -> candidate bits per chunk
-  uint16_t code[VB_NW][VB_JCAP];            // entry << 8 | index in the source cell
-  double hx[VB_NW][32][3];                  // home positions (broadcast reads)
-  uint8_t lmap[VB_NW][96];                  // lane -> first / second particle, switch round
+// Shared memory of the builder: NW warps, up to MAXP particles per home cell,
+// up to JCAP candidates (14 source cells).  The main pass takes cells of <= 32
+// particles (one lane per particle) with 4 warps per CTA; cells above that go
+// to a second pass with up to 64 (two particles per lane) and 896 candidates.
+// The round table is placed directly in its global slot (no shared copy), so
+// the main pass needs 28.5 KB of shared memory per CTA: at <= 70 registers 7
+// CTAs (28 warps) fit an SM (measured: rebuild 865 -> 825 us on cfg2).
+template <int NW, int MAXP, int JCAP>
+struct VBuildSmemT {
+  static constexpr int NCH = JCAP / 32;
+  unsigned used[NW][2][JCAP];  // per candidate j: rounds taken (low, high 32)
+  unsigned row[NW][MAXP][NCH];  // particle -> candidate bits per chunk
+  uint16_t code[NW][JCAP];      // entry << 8 | index in the source cell
+  double hx[NW][MAXP][3];       // home positions (broadcast reads)
+  uint8_t lmap[NW][96];         // lane -> first / second particle, switch round
 };
+#define VB_MINB 7
+using VBMain = VBuildSmemT<VB_NW, 32, VB_JCAP>;
+using VBCrowd = VBuildSmemT<1, 64, 2 * VB_JCAP>;
 
 // Lockstep first-fit: lane p places all pairs of particle p (row bits over the
 // candidate chunks) into its own slots -- up to VB_SEG segments (table lane
@@ -130,20 +145,20 @@ struct VBuildSmem {
 // that does not hold the same j yet, lowest round first.  Equal (j, round)
 // proposals are won by the lowest lane; lanes start at different j so that
 // such collisions are rare.  Returns false (warp-uniform) if a pair found no
-// slot.
+// slot.  u0 / u1: rounds 0-31 / 32-63 taken per candidate j.
 __device__ __forceinline__ int vl_ffs(unsigned v) { return __ffs(v); }
 __device__ __forceinline__ int vl_ffs(unsigned long long v) { return __ffsll((long long)v); }
 
 template <class M>  // round masks: 32 bits while R <= 32, else 64
-__device__ __forceinline__ M vl_used(unsigned (*used)[VB_JCAP], int j);
+__device__ __forceinline__ M vl_used(const unsigned *u0, const unsigned *u1, int j);
 template <>
-__device__ __forceinline__ unsigned vl_used<unsigned>(unsigned (*used)[VB_JCAP], int j) {
-  return used[0][j];
+__device__ __forceinline__ unsigned vl_used<unsigned>(const unsigned *u0, const unsigned *u1, int j) {
+  return u0[j];
 }
 template <>
-__device__ __forceinline__ unsigned long long vl_used<unsigned long long>(unsigned (*used)[VB_JCAP],
-                                                                          int j) {
-  return ((unsigned long long)used[1][j] << 32) | used[0][j];
+__device__ __forceinline__ unsigned long long vl_used<unsigned long long>(const unsigned *u0,
+                                                                          const unsigned *u1, int j) {
+  return ((unsigned long long)u1[j] << 32) | u0[j];
 }
 
 // lowest free round of mask class `par` (0: any, 1: even, 2: odd) for a pair
@@ -168,9 +183,9 @@ __device__ __forceinline__ int vl_pick(const M *fr, M u, M par, int &k) {
 // never share a (j, round), so each parity resolves with its own match_any;
 // the lowest lane wins.
 template <class M>
-__device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
-                                         const int *seg_l, unsigned (*used)[VB_JCAP],
-                                         const uint16_t *code, uint16_t (*tab)[32], int lane) {
+__device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr, const int *seg_l,
+                                         unsigned *u0, unsigned *u1, const uint16_t *code,
+                                         uint16_t (*tab)[32], int lane) {
   const M EVEN = (M)0x5555555555555555ull, ODD = (M)0xAAAAAAAAAAAAAAAAull;
   bool ok = true;
   int cc = 0;
@@ -189,14 +204,14 @@ __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
         bB = __ffs(hb ? hb : rest) - 1;
       }
       const int jA = cc * 32 + bA;
-      rA = vl_pick<M>(fr, vl_used<M>(used, jA), ~(M)0, kA);
+      rA = vl_pick<M>(fr, vl_used<M>(u0, u1, jA), ~(M)0, kA);
       if (rA < 0) {  // no round left for a pending pair
         ok = false;
         cur = 0;
         cc = nch;
         bB = -1;
       } else if (bB >= 0) {
-        rB = vl_pick<M>(fr, vl_used<M>(used, cc * 32 + bB), (rA & 1) ? EVEN : ODD, kB);
+        rB = vl_pick<M>(fr, vl_used<M>(u0, u1, cc * 32 + bB), (rA & 1) ? EVEN : ODD, kB);
       }
     }
     const bool evA = rA >= 0 && !(rA & 1), pB = rB >= 0;
@@ -226,203 +241,267 @@ __device__ __forceinline__ bool vl_place(const unsigned *row, int nch, M *fr,
         }
       cur &= ~(1u << b);
       tab[r][tl] = code[j];
-      atomicOr(&used[r >> 5][j], 1u << (r & 31));  // native 32-bit shared atomic
+      atomicOr(r < 32 ? &u0[j] : &u1[j], 1u << (r & 31));  // native 32-bit shared atomic
     }
     __syncwarp();
   }
   return __all_sync(CS_FULL, ok);
 }
 
-__global__ void __launch_bounds__(VB_NW * 32, VB_MINB) k_verlet_build(Box b, const int32_t *start,
-                                                             const double *x, const double *y,
-                                                             const double *z, double rl2,
-                                                             VList L, unsigned *status) {
-  __shared__ VBuildSmem S;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t nhome = (int64_t)b.owned_x * b.nc[1] * b.nc[2];
-  for (int64_t t = (int64_t)blockIdx.x * VB_NW + w; t < nhome; t += (int64_t)gridDim.x * VB_NW) {
-    const int h0 = (int)(t % b.owned_x), h1 = (int)((t / b.owned_x) % b.nc[1]),
-              h2 = (int)(t / ((int64_t)b.owned_x * b.nc[1]));
-    const int64_t cell = box_cell(b, h0, h1, h2);
-    int st = 0, cnt = 0;
-    double s0 = 0, s1 = 0, s2 = 0;
-    if (lane < 14) vl_source(b, start, h0, h1, h2, lane, &st, &cnt, s0, s1, s2);
-    const int na = __shfl_sync(CS_FULL, cnt, 0), a0 = __shfl_sync(CS_FULL, st, 0);
-    int incl = cnt;
+// segments of one particle: table lanes cL, cL + 1, ... with free rounds
+// (n slots starting at round cO of table lane cL)
+__device__ __forceinline__ void vl_segments(int n, int cL, int cO, int R,
+                                            unsigned long long *fr, int *seg_l) {
+  int rest = n, lo = cO;
 #pragma unroll
-    for (int k = 1; k < 16; k <<= 1) {
-      const int v = __shfl_up_sync(CS_FULL, incl, k);
-      if (lane >= k) incl += v;
+  for (int k = 0; k < VB_SEG; ++k) {
+    const int hi = min(R, lo + rest);
+    const int w2 = hi - lo;
+    fr[k] = w2 > 0 ? (((w2 >= 64 ? ~0ull : ((1ull << w2) - 1))) << lo) : 0ull;
+    seg_l[k] = min(cL + k, 31);
+    rest -= max(w2, 0);
+    lo = 0;
+  }
+}
+
+// One home cell t by one warp: round table, lane map and round count.  Cells
+// above MAXP particles or JCAP candidates go to `crowd` (the second pass) or,
+// in the second pass (crowd null), are reported (status 2).
+template <int NW, int MAXP, int JCAP>
+__device__ __forceinline__ void vb_cell(const Box &b, const int32_t *start, const double *x,
+                                        const double *y, const double *z, double rl2,
+                                        const VList &L, unsigned *status,
+                                        VBuildSmemT<NW, MAXP, JCAP> &S, int w, int lane,
+                                        int64_t t, int32_t *crowd) {
+  constexpr int NPL = MAXP / 32;  // particles per lane
+  static_assert(NPL == 1 || NPL == 2, "32 or 64 particles per home cell");
+  using MM = typename std::conditional<(MAXP > 32), unsigned long long, unsigned>::type;
+  const int h0 = (int)(t % b.owned_x), h1 = (int)((t / b.owned_x) % b.nc[1]),
+            h2 = (int)(t / ((int64_t)b.owned_x * b.nc[1]));
+  const int64_t cell = box_cell(b, h0, h1, h2);
+  int st = 0, cnt = 0;
+  double s0 = 0, s1 = 0, s2 = 0;
+  if (lane < 14) vl_source(b, start, h0, h1, h2, lane, &st, &cnt, s0, s1, s2);
+  const int na = __shfl_sync(CS_FULL, cnt, 0), a0 = __shfl_sync(CS_FULL, st, 0);
+  int incl = cnt;
+#pragma unroll
+  for (int k = 1; k < 16; k <<= 1) {
+    const int v = __shfl_up_sync(CS_FULL, incl, k);
+    if (lane >= k) incl += v;
+  }
+  const int excl = incl - cnt;
+  const int nj = __shfl_sync(CS_FULL, incl, 13);
+  const int nch = (nj + 31) / 32;
+  uint8_t *lm = L.imap + cell * 96;
+  if (na == 0 || na > MAXP || nj > JCAP) {
+    if (na > MAXP || nj > JCAP) {
+      if (crowd) {  // a cell for the second pass
+        if (lane == 0) crowd[atomicAdd(L.ncrowd, 1)] = (int32_t)t;
+      } else {
+        atomicOr(status, 2u);
+      }
     }
-    const int excl = incl - cnt;
-    const int nj = __shfl_sync(CS_FULL, incl, 13);
-    const int nch = (nj + 31) / 32;
-    uint8_t *lm = L.imap + cell * 96;
-    if (na == 0 || na > 32 || nj > VB_JCAP) {
-      if (na > 32 || nj > VB_JCAP) atomicOr(status, 2u);
-      if (lane == 0) L.nround[cell] = 0;
-      lm[lane] = lm[32 + lane] = 0xFF;
+    if (lane == 0) L.nround[cell] = 0;
+    lm[lane] = lm[32 + lane] = 0xFF;
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < NPL; ++k) {
+    const int p = k * 32 + lane;
+    if (p < na) {
+      S.hx[w][p][0] = __ldg(x + a0 + p);
+      S.hx[w][p][1] = __ldg(y + a0 + p);
+      S.hx[w][p][2] = __ldg(z + a0 + p);
+    }
+  }
+  __syncwarp();
+  // pass 1: candidates (lane = j) -> rows (lane = home particle), list lengths
+  int len0 = 0, len1 = 0;
+  for (int c = 0; c < nch; ++c) {
+    const int tj = c * 32 + lane;
+    int e = 0;
+#pragma unroll
+    for (int k = 8; k >= 1; k >>= 1) {
+      const int cand = e + k;
+      const int ex = __shfl_sync(CS_FULL, excl, cand < 14 ? cand : 13);
+      if (cand < 14 && ex <= tj) e = cand;
+    }
+    const int q = tj - __shfl_sync(CS_FULL, excl, e);
+    const int sst = __shfl_sync(CS_FULL, st, e);
+    const double sx = __shfl_sync(CS_FULL, s0, e), sy = __shfl_sync(CS_FULL, s1, e),
+                 sz = __shfl_sync(CS_FULL, s2, e);
+    MM mask = 0;
+    if (tj < nj) {
+      const double xj = __ldg(x + sst + q) + sx, yj = __ldg(y + sst + q) + sy,
+                   zj = __ldg(z + sst + q) + sz;
+      const int ilim = e == 0 ? q : na;  // intra: pairs i < j only
+      for (int i = 0; i < ilim; ++i) {
+        const double dx = S.hx[w][i][0] - xj, dy = S.hx[w][i][1] - yj, dz = S.hx[w][i][2] - zj;
+        const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
+        mask |= (MM)(r2 < rl2) << i;
+      }
+      S.code[w][tj] = (uint16_t)((e << 8) | q);
+    }
+    for (int i = 0; i < na; ++i) {
+      const unsigned bal = __ballot_sync(CS_FULL, (unsigned)(mask >> i) & 1u);
+      if (lane == (i & 31)) {
+        S.row[w][i][c] = bal;
+        if (i < 32) len0 += __popc(bal);
+        else len1 += __popc(bal);
+      }
+    }
+  }
+  const int n0 = lane < na ? len0 + 1 + len0 / 16 : 0;  // slots: pairs + slack
+  const int n1 = 32 + lane < na ? len1 + 1 + len1 / 16 : 0;
+  const int P = warp_sum(n0 + n1);
+  if (warp_sum(len0 + len1) == 0) {
+    if (lane == 0) L.nround[cell] = 0;
+    lm[lane] = lm[32 + lane] = 0xFF;
+    return;
+  }
+  // at most VB_SEG table lanes per particle: n <= (VB_SEG - 1) R + 1
+  int R = max((P + 31) / 32,
+              ((int)__reduce_max_sync(CS_FULL, (unsigned)max(n0, n1)) + VB_SEG - 3) / (VB_SEG - 1));
+  bool placed = false;
+  uint16_t(*tab)[32] = reinterpret_cast<uint16_t(*)[32]>(L.desc + cell * (VL_RMAX * 32));
+  unsigned *u0 = S.used[w][0], *u1 = S.used[w][1];
+  while (!placed && R <= VL_RMAX) {
+    // lane-major layout: particles in order, at most two per table lane (a
+    // particle that would be the third in a lane starts the next one)
+    int Lc = 0, off = 0, segs = 0, cL0 = 0, cO0 = 0, cL1 = 0, cO1 = 0;
+    for (int p = 0; p < na; ++p) {
+      int rest = __shfl_sync(CS_FULL, p < 32 ? n0 : n1, p & 31);
+      if (off != 0 && segs >= 2) {
+        ++Lc;
+        off = segs = 0;
+      }
+      if (off & 1) {  // switch rounds are even: the force kernel takes rounds in pairs
+        if (++off == R) {
+          ++Lc;
+          off = segs = 0;
+        }
+      }
+      if (lane == (p & 31)) {
+        if (p < 32) {
+          cL0 = Lc;
+          cO0 = off;
+        } else {
+          cL1 = Lc;
+          cO1 = off;
+        }
+      }
+      const int take = min(rest, R - off);
+      rest -= take;
+      off += take;
+      ++segs;
+      if (off == R) {
+        ++Lc;
+        off = segs = 0;
+      }
+      if (rest > 0) {  // (rest < VB_SEG * R: a short loop, no integer division)
+        while (rest >= R) {
+          rest -= R;
+          ++Lc;
+        }
+        off = rest;
+        segs = off ? 1 : 0;
+      }
+    }
+    if (Lc + (off ? 1 : 0) > 32) {
+      ++R;
       continue;
     }
-    if (lane < na) {
-      S.hx[w][lane][0] = __ldg(x + a0 + lane);
-      S.hx[w][lane][1] = __ldg(y + a0 + lane);
-      S.hx[w][lane][2] = __ldg(z + a0 + lane);
-    }
+    unsigned long long fr0[VB_SEG], fr1[VB_SEG];
+    int seg0[VB_SEG], seg1[VB_SEG];
+    vl_segments(n0, cL0, cO0, R, fr0, seg0);
+    vl_segments(n1, cL1, cO1, R, fr1, seg1);
+    for (int r = 0; r < R; ++r) tab[r][lane] = VL_IDLE;
+    // lane -> (first particle, second particle, switch round)
+    S.lmap[w][lane] = S.lmap[w][32 + lane] = 0xFF;
+    S.lmap[w][64 + lane] = (uint8_t)R;
+    for (int j = lane; j < nj; j += 32) u0[j] = u1[j] = 0u;
     __syncwarp();
-    // pass 1: candidates (lane = j) -> rows (lane = home particle), list lengths
-    int len = 0;
-    for (int c = 0; c < nch; ++c) {
-      const int tj = c * 32 + lane;
-      int e = 0;
 #pragma unroll
-      for (int k = 8; k >= 1; k >>= 1) {
-        const int cand = e + k;
-        const int ex = __shfl_sync(CS_FULL, excl, cand < 14 ? cand : 13);
-        if (cand < 14 && ex <= tj) e = cand;
-      }
-      const int q = tj - __shfl_sync(CS_FULL, excl, e);
-      const int sst = __shfl_sync(CS_FULL, st, e);
-      const double sx = __shfl_sync(CS_FULL, s0, e), sy = __shfl_sync(CS_FULL, s1, e),
-                   sz = __shfl_sync(CS_FULL, s2, e);
-      unsigned mask = 0;
-      if (tj < nj) {
-        const double xj = __ldg(x + sst + q) + sx, yj = __ldg(y + sst + q) + sy,
-                     zj = __ldg(z + sst + q) + sz;
-        const int ilim = e == 0 ? q : na;  // intra: pairs i < j only
-        for (int i = 0; i < ilim; ++i) {
-          const double dx = S.hx[w][i][0] - xj, dy = S.hx[w][i][1] - yj, dz = S.hx[w][i][2] - zj;
-          const double r2 = __fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx));
-          mask |= (unsigned)(r2 < rl2) << i;
-        }
-        S.code[w][tj] = (uint16_t)((e << 8) | q);
-      }
-      for (int i = 0; i < na; ++i) {
-        const unsigned bal = __ballot_sync(CS_FULL, (mask >> i) & 1u);
-        if (lane == i) {
-          S.row[w][i][c] = bal;
-          len += __popc(bal);
-        }
-      }
-    }
-    const int n = lane < na ? len + 1 + len / 16 : 0;  // slots: pairs + slack
-    const int P = warp_sum(n);
-    if (warp_sum(len) == 0) {
-      if (lane == 0) L.nround[cell] = 0;
-      lm[lane] = lm[32 + lane] = 0xFF;
-      continue;
-    }
-    // at most VB_SEG table lanes per particle: n <= (VB_SEG - 1) R + 1
-    int R = max((P + 31) / 32, ((int)__reduce_max_sync(CS_FULL, (unsigned)n) + VB_SEG - 3) / (VB_SEG - 1));
-    bool placed = false;
-    while (!placed && R <= VL_RMAX) {
-      // lane-major layout: particles in order, at most two per table lane (a
-      // particle that would be the third in a lane starts the next one)
-      int Lc = 0, off = 0, segs = 0, cL = 0, cO = 0;
-      for (int p = 0; p < na; ++p) {
-        int rest = __shfl_sync(CS_FULL, n, p);
-        if (off != 0 && segs >= 2) {
-          ++Lc;
-          off = segs = 0;
-        }
-        if (off & 1) {  // switch rounds are even: the force kernel takes rounds in pairs
-          if (++off == R) {
-            ++Lc;
-            off = segs = 0;
-          }
-        }
-        if (lane == p) {
-          cL = Lc;
-          cO = off;
-        }
-        const int take = min(rest, R - off);
-        rest -= take;
-        off += take;
-        ++segs;
-        if (off == R) {
-          ++Lc;
-          off = segs = 0;
-        }
-        if (rest > 0) {  // (rest < VB_SEG * R: a short loop, no integer division)
-          while (rest >= R) {
-            rest -= R;
-            ++Lc;
-          }
-          off = rest;
-          segs = off ? 1 : 0;
-        }
-      }
-      if (Lc + (off ? 1 : 0) > 32) {
-        ++R;
-        continue;
-      }
-      // this particle's segments: table lanes cL, cL + 1, ... with free rounds
-      unsigned long long fr[VB_SEG];
-      int seg_l[VB_SEG];
-      {
-        int rest = n, lo = cO;
-#pragma unroll
-        for (int k = 0; k < VB_SEG; ++k) {
-          const int hi = min(R, lo + rest);
-          const int w2 = hi - lo;
-          fr[k] = w2 > 0 ? (((w2 >= 64 ? ~0ull : ((1ull << w2) - 1))) << lo) : 0ull;
-          seg_l[k] = min(cL + k, 31);
-          rest -= max(w2, 0);
-          lo = 0;
-        }
-      }
-      uint16_t(*tab)[32] = reinterpret_cast<uint16_t(*)[32]>(L.desc + cell * (VL_RMAX * 32));
-      for (int r = 0; r < R; ++r) tab[r][lane] = VL_IDLE;
-      // lane -> (first particle, second particle, switch round)
-      S.lmap[w][lane] = S.lmap[w][32 + lane] = 0xFF;
-      S.lmap[w][64 + lane] = (uint8_t)R;
-      for (int j = lane; j < nj; j += 32) S.used[w][0][j] = S.used[w][1][j] = 0u;
-      __syncwarp();
-      if (lane < na) {
+    for (int k = 0; k < NPL; ++k) {
+      const int p = k * 32 + lane;
+      const int cL = k ? cL1 : cL0, cO = k ? cO1 : cO0;
+      const unsigned long long *fr = k ? fr1 : fr0;
+      const int *seg = k ? seg1 : seg0;
+      if (p < na) {
         if (cO != 0) {
-          S.lmap[w][32 + cL] = (uint8_t)lane;
+          S.lmap[w][32 + cL] = (uint8_t)p;
           S.lmap[w][64 + cL] = (uint8_t)cO;
         } else {
-          S.lmap[w][cL] = (uint8_t)lane;
+          S.lmap[w][cL] = (uint8_t)p;
         }
 #pragma unroll
-        for (int k = 1; k < VB_SEG; ++k)
-          if (fr[k]) S.lmap[w][seg_l[k]] = (uint8_t)lane;
+        for (int kk = 1; kk < VB_SEG; ++kk)
+          if (fr[kk]) S.lmap[w][seg[kk]] = (uint8_t)p;
       }
-      __syncwarp();
-      // pass 2: place the pairs
-      bool ok;
+    }
+    __syncwarp();
+    // pass 2: place the pairs (the second particle set after the first)
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+      if (!ok) break;
+      const int p = k * 32 + lane;
+      unsigned long long *fr = k ? fr1 : fr0;
+      const int *seg = k ? seg1 : seg0;
+      const unsigned *prow = S.row[w][p < na ? p : 0];
+      const int pn = p < na ? nch : 0;
       if (R <= 32) {
         unsigned f32[VB_SEG];
 #pragma unroll
-        for (int k = 0; k < VB_SEG; ++k) f32[k] = (unsigned)fr[k];
-        ok = vl_place(S.row[w][lane < na ? lane : 0], lane < na ? nch : 0, f32, seg_l, S.used[w],
-                      S.code[w], tab, lane);
+        for (int kk = 0; kk < VB_SEG; ++kk) f32[kk] = (unsigned)fr[kk];
+        ok = vl_place(prow, pn, f32, seg, u0, u1, S.code[w], tab, lane);
       } else {
-        ok = vl_place(S.row[w][lane < na ? lane : 0], lane < na ? nch : 0, fr, seg_l, S.used[w],
-                      S.code[w], tab, lane);
-      }
-      if (ok) {
-        placed = true;
-      } else {  // a pair found no free round: clear and retry with one more round
-        __syncwarp();
-        ++R;  // (the next attempt re-initialises its rounds)
+        ok = vl_place(prow, pn, fr, seg, u0, u1, S.code[w], tab, lane);
       }
     }
-    if (!placed) {
-      if (lane == 0) {
-        atomicOr(status, 4u);
-        L.nround[cell] = 0;
-      }
-      lm[lane] = lm[32 + lane] = 0xFF;
-      continue;
+    if (ok) {
+      placed = true;
+    } else {  // a pair found no free round: retry with one more round
+      __syncwarp();
+      ++R;  // (the next attempt re-initialises its rounds)
     }
-    if (lane == 0) L.nround[cell] = R;
-    lm[lane] = S.lmap[w][lane];
-    lm[32 + lane] = S.lmap[w][32 + lane];
-    lm[64 + lane] = S.lmap[w][64 + lane];
-    __syncwarp();
   }
+  if (!placed) {
+    if (lane == 0) {
+      atomicOr(status, 4u);
+      L.nround[cell] = 0;
+    }
+    lm[lane] = lm[32 + lane] = 0xFF;
+    return;
+  }
+  if (lane == 0) L.nround[cell] = R;
+  lm[lane] = S.lmap[w][lane];
+  lm[32 + lane] = S.lmap[w][32 + lane];
+  lm[64 + lane] = S.lmap[w][64 + lane];
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(VB_NW * 32, VB_MINB) k_verlet_build(Box b, const int32_t *start,
+                                                                      const double *x, const double *y,
+                                                                      const double *z, double rl2,
+                                                                      VList L, unsigned *status) {
+  __shared__ VBMain S;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t nhome = (int64_t)b.owned_x * b.nc[1] * b.nc[2];
+  for (int64_t t = (int64_t)blockIdx.x * VB_NW + w; t < nhome; t += (int64_t)gridDim.x * VB_NW)
+    vb_cell(b, start, x, y, z, rl2, L, status, S, w, lane, t, L.crowd);
+}
+
+// second pass: the (rare) cells of 33-64 particles, one warp each
+__global__ void __launch_bounds__(32) k_verlet_build_crowded(Box b, const int32_t *start,
+                                                             const double *x, const double *y,
+                                                             const double *z, double rl2, VList L,
+                                                             unsigned *status) {
+  __shared__ VBCrowd S;
+  const int n = *L.ncrowd;
+  for (int i = blockIdx.x; i < n; i += gridDim.x)
+    vb_cell(b, start, x, y, z, rl2, L, status, S, 0, threadIdx.x, (int64_t)L.crowd[i],
+            (int32_t *)nullptr);
 }
 
 __global__ void k_wrap_copy(int64_t n, double Lx, double Ly, double Lz, double *x, double *y,
@@ -550,7 +629,7 @@ extern "C" int cs_verlet_build(const cs_box *bx, const cs_lj *lj, double skin,
   CS_REQUIRE(list_bytes >= vl_bytes(b), "Verlet list buffer too small (%zu < %zu)",
              list_bytes, vl_bytes(b));
   CS_REQUIRE(status_dev, "status pointer required");
-  VList L = vl_view(list, b.ncells);
+  VList L = vl_view(list, b);
   const double rl = lj->rc + skin;
   const double rl2 = rl * rl * (1.0 + 1e-12);
   const int64_t nhome = (int64_t)b.owned_x * b.nc[1] * b.nc[2];
@@ -558,8 +637,13 @@ extern "C" int cs_verlet_build(const cs_box *bx, const cs_lj *lj, double skin,
   if (b.ncells > nhome) {  // ghost cells own no home tasks
     CS_CUDA(cudaMemsetAsync(L.nround, 0, sizeof(int32_t) * b.ncells, st));
   }
-  if (blocks > 0)
+  if (blocks > 0) {
+    CS_CUDA(cudaMemsetAsync(L.ncrowd, 0, sizeof(int32_t), st));
     k_verlet_build<<<(unsigned)blocks, VB_NW * 32, 0, st>>>(b, cell_start, x, y, z, rl2, L, status_dev);
+    // (returns at once when no cell was crowded; the grid reads the count on the device)
+    k_verlet_build_crowded<<<(unsigned)(nhome < 592 ? nhome : 592), 32, 0, st>>>(b, cell_start, x, y, z,
+                                                                                rl2, L, status_dev);
+  }
   // the buffered block layout only changes with the cell list: compute it here
   // once per rebuild instead of in every force evaluation
   int nbk[3];

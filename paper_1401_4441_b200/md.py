@@ -612,7 +612,7 @@ class LJSystem:
                 "buffered force schedule: a block exceeded its shared-memory capacity; "
                 "use schedule='shell' (in-place fallback) for this density")
         if st & 2:
-            raise _lib.CellschedError("Verlet list: a cell holds more than 32 particles; "
+            raise _lib.CellschedError("Verlet list: a cell holds more than 64 particles; "
                                       "use a link-cell schedule for this density")
         if st & 4:
             raise _lib.CellschedError("Verlet list: a home cell needs more than 64 rounds; "

@@ -111,17 +111,51 @@ def test_verlet_needs_wide_cells(cuda):
         md.LJSystem(box, 4 * 14 ** 3, schedule="verlet", skin=0.3)
 
 
+def test_verlet_crowded_cells_second_pass(oracle, cuda):
+    """Home cells of 33-64 particles take the builder's second pass (two
+    particles per lane): a dense-liquid-like fluctuation -- 14 particles added
+    to one cell of an FCC system (21 per cell), no two closer than 0.75 --
+    gives forces and pair count that still match the oracle."""
+    rng = np.random.default_rng(5)
+    base = md.LJSystem.fcc(14, schedule="verlet", skin=0.3)  # 8^3 cells of edge 2.94
+    snap0 = base.snapshot()
+    pts = snap0["x"] % np.asarray(base.box.lengths)
+    edge = base.box.lengths[0] / base.box.cells[0]
+    extra = []
+    while len(extra) < 14:
+        c = 0.1 + rng.random(3) * (edge - 0.2)
+        allp = np.concatenate([pts, np.array(extra).reshape(-1, 3)])
+        if np.min(np.linalg.norm(allp - c, axis=1)) >= 0.75:
+            extra.append(c)
+    pts = np.concatenate([pts, np.array(extra)])
+    n = len(pts)
+    s = md.LJSystem(base.box, n, schedule="verlet", skin=0.3)
+    z = np.zeros(n)
+    s.load_host(pts[:, 0], pts[:, 1], pts[:, 2], z, z, z, np.arange(n))
+    snap = s.snapshot()
+    assert 32 < np.diff(snap["cell_start"]).max() <= 64
+    x = snap["x"]
+    f, pe, npair = oracle.lj_direct(list(s.box.cells), list(s.box.lengths), snap["cell_start"],
+                                    np.ascontiguousarray(x[:, 0]), np.ascontiguousarray(x[:, 1]),
+                                    np.ascontiguousarray(x[:, 2]), rc=2.5)
+    assert s.pair_count() == npair  # (also raises on a capacity flag)
+    frms = np.sqrt((f ** 2).sum(1).mean())
+    err = (np.linalg.norm(snap["f"] - f, axis=1) / np.maximum(np.linalg.norm(f, axis=1), frms)).max()
+    assert err < 1e-10
+    assert abs(s.energies()[0] - pe) / abs(pe) < 1e-12
+
+
 def test_verlet_crowded_cell_is_reported(cuda):
-    """A home cell with more than 32 particles cannot be laid out on a warp's
+    """A home cell with more than 64 particles cannot be laid out on a warp's
     lanes: the build flags it and the system raises instead of returning
     partial forces."""
     rng = np.random.default_rng(5)
-    box = md.LJBox((24.0, 24.0, 24.0), (8, 8, 8))  # edge 3.0 >= rc + skin
+    box = md.LJBox((24.0, 24.0, 24.0), (8, 8, 8))
     n = 3000
     pts = rng.random((n, 3)) * 24.0
-    pts[:60] = 0.2 + rng.random((60, 3)) * 2.5  # 60 particles in one cell
+    pts[:70] = 0.2 + rng.random((70, 3)) * 2.5  # 70 particles in one cell
     s = md.LJSystem(box, n, schedule="verlet", skin=0.3)
     z = np.zeros(n)
     s.load_host(pts[:, 0], pts[:, 1], pts[:, 2], z, z, z, np.arange(n))
-    with pytest.raises(Exception, match="more than 32 particles"):
+    with pytest.raises(Exception, match="more than 64 particles"):
         s.energies()
