@@ -523,8 +523,9 @@ class LJSystem:
             return 2 + force + 1 + (3 if energy else 0)
         return 1 + build + force + 1 + (3 if energy else 0)
 
-    REBUILD_LAUNCHES = 15  # wrap, rebin (count, scan x3, scatter, sort-gather), copy-back,
-    #                        round tables, reference copy, block sizes, scan x3, block tables
+    REBUILD_LAUNCHES = 16  # wrap, rebin (count, scan x3, scatter, sort-gather), copy-back,
+    #                        round tables (main + crowded-cell pass), reference copy, block
+    #                        sizes, scan x3, block tables
 
     def candidate_pairs_dev(self):
         """Half-shell candidate pairs C of the current cell list as a device
