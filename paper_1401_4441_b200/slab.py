@@ -295,8 +295,6 @@ class CudaSlabEngine:
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         nx, ny, nz = box.cells
         owned = layout.owned
-        per_plane = max(1, int(round(4.0 * 1.0)))  # placeholder, refined below
-        dens = None
         self.box_length_x = box.lengths[0]
         b = _lib.CsBox()
         b.nc[0], b.nc[1], b.nc[2] = owned + 1, ny, nz
@@ -316,7 +314,6 @@ class CudaSlabEngine:
         self.n_ghost = 0
         self.ncells_local = (owned + 1) * ny * nz
         self.plane_cells = ny * nz
-        del per_plane, dens
 
     # -- allocation (capacity in particles, owned + ghost) --------------------
     def _alloc(self, cap):
