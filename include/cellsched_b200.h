@@ -333,6 +333,29 @@ int cs_set_ghost_plane(const cs_box *b, int64_t n_owned, const int32_t *ghost_co
                        double *y, double *z, double *fx, double *fy, double *fz, void *ws,
                        size_t ws_bytes, void *stream);
 
+/* ============ a11 / f3: worker-pool model (list scheduling) on the device =====
+ * One persistent CTA, ready set as a bitmap scanned forward (the smallest ready
+ * id never decreases), unit task durations, ready tasks handed to workers in
+ * ascending id order.  Both synchronise (the makespan is returned on the host). */
+/* simulate (schedsim.py:63-90): successor CSR sptr[ntasks+1] / succ[nedges] of
+ * a forward-edge graph; start[t] = time step task t runs; *makespan_host =
+ * SimResult.makespan.  CS_ECYCLE if the schedule stalls (schedsim.py:88-89). */
+size_t cs_listsched_ws_bytes(int64_t ntasks);
+int cs_simulate_static(int64_t ntasks, int64_t nedges, const int64_t *sptr, const int32_t *succ,
+                       int64_t workers, int32_t *start, int64_t *makespan_host, void *ws,
+                       size_t ws_bytes, void *stream);
+/* simulate_dynamic on a NestedPlan (schedsim.py:93-163, taskgen.py:279-325):
+ * order_host = n offsets x dim int8, intra first.  Task arrays (capacity >=
+ * cells * n): home cell, chain entry (index into order), spawning parent (-1 =
+ * initial task), the realized predecessors pred_a < pred_b (-1 = none; the
+ * edges of SimResult.graph, depgraph.py:28-49 applied at spawn time) and the
+ * start step.  *ntasks_host = realized tasks (the spawn log length). */
+size_t cs_nested_ws_bytes(const cs_grid *g, int n);
+int cs_simulate_nested(const cs_grid *g, const int8_t *order_host, int n, int64_t workers,
+                       int32_t *home, int16_t *entry, int32_t *parent, int32_t *pred_a,
+                       int32_t *pred_b, int32_t *start, int64_t capacity, int64_t *ntasks_host,
+                       int64_t *makespan_host, void *ws, size_t ws_bytes, void *stream);
+
 /* FP64 pipe probe used by bench.py to measure the FP64 roofline peak:
  * blocks x 256 threads x iters x 256 flops (DFMA = 2 flops). */
 int cs_probe_dfma(int blocks, int iters, double *out, void *stream);

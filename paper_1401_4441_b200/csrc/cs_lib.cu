@@ -6,6 +6,7 @@
 #include "cs_sched.cuh"
 #include "cs_payload.cuh"
 #include "cs_generic.cuh"
+#include "cs_listsched.cuh"
 #include "cs_md.cuh"
 #include "cs_force.cuh"
 #include "cs_force2.cuh"
