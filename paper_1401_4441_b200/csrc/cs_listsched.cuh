@@ -332,7 +332,7 @@ size_t cs_nested_ws_bytes(const cs_grid *g, int n) {
   int64_t cells = 1;
   for (int k = 0; g && k < g->dim; ++k) cells *= g->ext[k] > 0 ? g->ext[k] : 1;
   const int64_t cap = cells * (n > 0 ? n : 1);
-  return cs_ws_slice(4 * cap) * 4 + cs_ws_slice(4 * cells) +
+  return cs_ws_slice(4 * cap) * 6 + cs_ws_slice(4 * cells) +
          cs_ws_slice(4 * ((cap + 31) / 32)) + cs_ws_slice(sizeof(LsState));
 }
 

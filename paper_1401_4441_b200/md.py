@@ -153,6 +153,28 @@ def liquid_vapour_positions(cells=(64, 64, 192), edge: float = 2.5, rho_liquid: 
     return tuple(float(v) for v in L), np.concatenate([liquid, vap])
 
 
+def verlet_box(lengths, rc: float, skin: float):
+    """Cells for the Verlet schedules: edge >= rc + skin, a multiple of 4 per
+    axis (the 2x2x2 block colouring), at least 4.  A box too small for 4
+    cells of rc + skin (cfg1: L = 10.08, rc + 0.35 = 2.85) keeps 4 cells and
+    narrows the skin to the widest the cells allow (cfg1: L/4 - rc = 0.0194),
+    with a UserWarning -- the list is then rebuilt every few steps.  Returns
+    (box, skin)."""
+    import warnings
+
+    fit = [int(math.floor(L / (rc + skin))) for L in lengths]
+    box = LJBox(tuple(lengths), tuple(max(4, c - c % 4) for c in fit))
+    edge = min(box.cell_edge)
+    if edge < (rc + skin) * (1 - 1e-12):
+        if edge <= rc:
+            raise ValueError(f"box {box.lengths} is too small for 4 cells of edge > rc = {rc}")
+        narrowed = edge - rc
+        warnings.warn(f"4 cells of edge {edge:.6g} cannot hold rc + skin = {rc + skin:.6g}; "
+                      f"using skin {narrowed:.6g}", stacklevel=3)
+        skin = narrowed
+    return box, skin
+
+
 def choose_block(cells, density_per_cell: float = 13.5, cap: int = 2048):
     """Largest block (By, Bz >= 2) whose 2x2x2 colour passes still fill the
     GPU (>= 296 CTAs per pass) and whose footprint fits the staging cap."""
@@ -275,10 +297,8 @@ class LJSystem:
         Verlet schedules bin on cells of edge >= rc + skin."""
         verlet = schedule in VERLET_SCHEDULES
         box, nuc, a = fcc_box(n_unit_cells, density, params.rc + (skin if verlet else 0.0))
-        if verlet and any(c % 4 for c in box.cells):
-            # the 2x2x2 block colouring needs multiples of 4 cells: widen the cells
-            cells = tuple(max(4, c - c % 4) for c in box.cells)
-            box = LJBox(box.lengths, cells)
+        if verlet:
+            box, skin = verlet_box(box.lengths, params.rc, skin)
         n = 4 * nuc[0] * nuc[1] * nuc[2]
         s = cls(box, n, params, schedule, block, skin=skin)
         s.dt = dt
@@ -297,8 +317,7 @@ class LJSystem:
         verlet = schedule in VERLET_SCHEDULES
         box = LJBox(L, cells)
         if verlet:
-            box = LJBox.for_cutoff(L, params.rc + skin)
-            box = LJBox(L, tuple(max(4, c - c % 4) for c in box.cells))
+            box, skin = verlet_box(L, params.rc, skin)
         s = cls(box, len(xyz), params, schedule, block, skin=skin)
         s.dt = dt
         s.seed_positions(xyz, temperature, seed)
