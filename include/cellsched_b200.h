@@ -49,6 +49,9 @@ typedef struct cs_grid {
 int cs_abi_version(void);
 const char *cs_last_error(void);
 int cs_device_synchronize(void);
+/* stream-ordered byte fill of device memory (cudaMemsetAsync; a memset node
+ * when captured): clears per-step result words without framework kernels */
+int cs_memset_async(void *dst, int value, size_t bytes, void *stream);
 
 /* ===================== K4: task streams and serialization depth ========== */
 enum { CS_STREAM_BASIC = 0, CS_STREAM_LOOPEX = 1 };
@@ -204,6 +207,12 @@ int cs_build_cells(int64_t n, const cs_box *b, const double *x, const double *y,
                    const int32_t *id, double *xo, double *yo, double *zo, double *vxo,
                    double *vyo, double *vzo, int32_t *ido, double *fxo, double *fyo,
                    double *fzo, int32_t *cell_start, void *ws, size_t ws_bytes, void *stream);
+/* Range flag of the last cs_build_cells on workspace `ws` (same n, box):
+ * *flag_host = 1 if a particle lay outside the local cell range and was
+ * clamped into an edge cell (slab: a particle that should have migrated).
+ * Synchronises. */
+int cs_bin_errors(int64_t n, const cs_box *b, const void *ws, size_t ws_bytes, int *flag_host,
+                  void *stream);
 
 /* K2: fp64 LJ half-shell forces with Newton-3 reaction writes under a
  * conflict-free schedule; f must be zeroed by the caller (cs_build_cells

@@ -41,6 +41,17 @@ int cs_check_launch(const char *what);  // cudaGetLastError -> status
 
 static inline cudaStream_t cs_stream(void *s) { return (cudaStream_t)s; }
 
+// one-time per-device set-up (constant tables, kernel attributes, occupancy
+// caps) is cached per device: __constant__ memory and function attributes
+// are per device, so a process that calls the library on a second GPU must
+// set them up there too
+#define CS_MAX_DEVICES 64
+static inline int cs_device_index() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0) d = 0;
+  return d < CS_MAX_DEVICES ? d : CS_MAX_DEVICES - 1;
+}
+
 // ------------------------------------------------------------- workspace --
 // bump allocator over the caller workspace (256-byte aligned slices)
 struct cs_ws {

@@ -48,7 +48,7 @@ struct ForceArgs {
 };
 
 // level (0..26) -> (stencil entry, parity); level 0 = intra
-__device__ __forceinline__ void level_entry(int level, int *e, int *par) {
+__host__ __device__ __forceinline__ void level_entry(int level, int *e, int *par) {
   *e = level == 0 ? 0 : (level + 1) >> 1;
   *par = level == 0 ? 0 : (level + 1) & 1;
 }
@@ -448,9 +448,25 @@ static int lj_forces_impl(const cs_box *bx, const cs_lj *lj, int sched, int64_t 
                                           : (sched == CS_SCHED_DATAFLOW ? SH_DATAFLOW : SH_COLOUR),
                                true, &w, npart, status_dev, st));
   } else if (sched == CS_SCHED_LOOPEX) {
+    // the level sets are write-disjoint only if no periodic axis wraps with
+    // an odd extent (taskgen.py:210-215 warns for the same case)
+    const int hext[3] = {A.b.owned_x, A.b.nc[1], A.b.nc[2]};
+    for (int k = 0; k < 3; ++k)
+      CS_REQUIRE(!A.b.per[k] || hext[k] % 2 == 0,
+                 "loop-exchange colour passes need even periodic extents (axis %d has %d cells)", k,
+                 hext[k]);
+    int8_t st3[14 * 3];
+    int nst;
+    cs_host_canonical_stencil(3, st3, &nst);
     for (int level = 0; level < 27; ++level) {
-      int64_t ntask = (int64_t)A.b.owned_x * A.b.nc[1] * A.b.nc[2];  // upper bound
-      if (level > 0) ntask = (ntask + 1) / 2 + (int64_t)A.b.nc[1] * A.b.nc[2];
+      int e, par;
+      level_entry(level, &e, &par);
+      int ax = 0;  // highest axis with a nonzero offset component (the parity axis)
+      for (int k = 0; k < 3; ++k)
+        if (st3[3 * e + k]) ax = k;
+      int64_t ntask = 1;  // the kernel's task grid m[] of this level
+      for (int k = 0; k < 3; ++k) ntask *= (level > 0 && k == ax) ? (hext[k] - par + 1) >> 1 : hext[k];
+      if (ntask == 0) continue;
       unsigned blocks = (unsigned)((ntask * 32 + 127) / 128);
       if (energy)
         k_force_loopex<true><<<blocks, 128, 0, st>>>(A, level);
@@ -461,13 +477,14 @@ static int lj_forces_impl(const cs_box *bx, const cs_lj *lj, int sched, int64_t 
     CS_TRY(block_grid(A.b, A.nbk));
     A.cap = force_cap(A.b);
     size_t smem = sizeof(double) * 3 * A.cap;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static size_t attr_smem[CS_MAX_DEVICES];  // largest dynamic shared memory enabled so far
+    const int dev = cs_device_index();
+    if (smem > attr_smem[dev]) {
       CS_CUDA(cudaFuncSetAttribute(k_force_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       CS_CUDA(cudaFuncSetAttribute(k_force_block<false>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_set = true;
+      attr_smem[dev] = smem;
     }
     for (int colour = 0; colour < 8; ++colour) {
       int kc[3] = {colour & 1, (colour >> 1) & 1, (colour >> 2) & 1};

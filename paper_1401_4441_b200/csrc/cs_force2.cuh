@@ -1145,15 +1145,16 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, int mode, bool v
   SA.vtab = A.vl_tab;
   CS_TRY(build_merge_table(B, &SA.mt));
   const size_t smem = verlet ? sizeof(ShellSmemVL) : sizeof(ShellSmem);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[CS_MAX_DEVICES];
+  const int devi = cs_device_index();
+  if (!attr[devi]) {
     for (int v = 0; v < 12; ++v) {
       const bool vl = v >= 6;
       const size_t sm = vl ? sizeof(ShellSmemVL) : sizeof(ShellSmem);
       CS_CUDA(cudaFuncSetAttribute(shell_kernel(v & 1, (v % 6) / 2, vl),
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     }
-    attr = true;
+    attr[devi] = true;
   }
   const ShellKernel kern = shell_kernel(energy, mode, verlet);
   if (mode == SH_DATAFLOW) {
@@ -1169,16 +1170,16 @@ static int launch_shell_passes(const ForceArgs &A, bool energy, int mode, bool v
       for (int k = 0; k < 3; ++k) cnt *= (A.nbk[k] - ((c >> k) & 1) + 1) >> 1;
       SA.coff[c + 1] = SA.coff[c] + cnt;
     }
-    static int grid_cap[2] = {0, 0};
-    if (!grid_cap[verlet]) {
+    static int grid_cap[CS_MAX_DEVICES][2];
+    if (!grid_cap[devi][verlet]) {
       int per_sm = 0, dev = 0, nsm = 0;
       CS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SH_NW * 32, smem));
       CS_CUDA(cudaGetDevice(&dev));
       CS_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-      grid_cap[verlet] = max(1, per_sm) * nsm;
+      grid_cap[devi][verlet] = max(1, per_sm) * nsm;
     }
     CS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * (nblocks + 1), st));
-    const unsigned grid = (unsigned)(nblocks < grid_cap[verlet] ? nblocks : grid_cap[verlet]);
+    const unsigned grid = (unsigned)(nblocks < grid_cap[devi][verlet] ? nblocks : grid_cap[devi][verlet]);
     kern<<<grid, SH_NW * 32, smem, st>>>(SA, -1);
     return cs_check_launch("force_dataflow");
   }

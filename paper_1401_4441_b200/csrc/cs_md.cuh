@@ -273,9 +273,27 @@ extern "C" int cs_build_cells(int64_t n, const cs_box *bx, const double *x, cons
   return cs_check_launch("build_cells");
 }
 
-// range errors of the last build (slab mode: particles that must migrate)
-// are reported through cs_bin_errors; kept separate so the build stays
-// free of host synchronisation.
+// Range flag of the last cs_build_cells on this workspace: 1 if a particle
+// lay outside the local cell range (a slab particle that should have
+// migrated, or an unwrapped position) and was clamped into an edge cell.
+// Kept out of the build itself so the build never synchronises; reads the
+// flag with one device->host copy.
+extern "C" int cs_bin_errors(int64_t n, const cs_box *bx, const void *ws, size_t ws_bytes,
+                             int *flag_host, void *stream) {
+  Box b;
+  CS_TRY(make_box(bx, &b));
+  cs_ws w(const_cast<void *>(ws), ws_bytes);  // the build's slice layout
+  CS_WS_TAKE(w, int32_t, cell_of, n + 1);
+  CS_WS_TAKE(w, int32_t, slot, n + 1);
+  CS_WS_TAKE(w, int32_t, src, n + 1);
+  CS_WS_TAKE(w, int32_t, count, b.ncells + 1);
+  CS_WS_TAKE(w, int, err, 16);
+  (void)cell_of, (void)slot, (void)src, (void)count;
+  cudaStream_t st = cs_stream(stream);
+  CS_CUDA(cudaMemcpyAsync(flag_host, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CS_CUDA(cudaStreamSynchronize(st));
+  return CS_OK;
+}
 
 // ------------------------------------------------------------ K3: Verlet --
 __global__ void k_kick(int64_t n, double hdtm, const double *fx, const double *fy,

@@ -612,10 +612,11 @@ extern "C" int cs_stream_depth(const cs_grid *g, int strategy, int n, int64_t nt
   ring = ring && ring_smem <= 200 * 1024;
   if (ring) {
     CS_WS_TAKE(w, int32_t, parked, (int64_t)e3[0] * e3[1]);
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[CS_MAX_DEVICES];
+    const int dev = cs_device_index();
+    if (!attr[dev]) {
       CS_CUDA(cudaFuncSetAttribute(k_depth_planes, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
+      attr[dev] = true;
     }
     k_depth_planes<<<1, 32, ring_smem, st>>>(e3[0], e3[1], e3[2], nper, nbr, level, parked, scalars);
     CS_TRY(cs_check_launch("depth_planes"));

@@ -28,6 +28,14 @@ extern "C" int cs_device_synchronize(void) {
   CS_CUDA(cudaDeviceSynchronize());
   return CS_OK;
 }
+// stream-ordered fill (captured as a memset node inside CUDA graphs): the
+// per-step result words are cleared through the C ABI, not by torch kernels
+extern "C" int cs_memset_async(void *dst, int value, size_t bytes, void *stream) {
+  if (bytes == 0) return CS_OK;
+  CS_REQUIRE(dst, "cs_memset_async: null destination");
+  CS_CUDA(cudaMemsetAsync(dst, value, bytes, cs_stream(stream)));
+  return CS_OK;
+}
 
 // ------------------------------------------------------- canonical stencil --
 void cs_host_canonical_stencil(int dim, int8_t *out, int *n) {
@@ -53,9 +61,10 @@ void cs_host_canonical_stencil(int dim, int8_t *out, int *n) {
   *n = m;
 }
 
-static bool g_stencil_uploaded = false;
+static bool g_stencil_uploaded[CS_MAX_DEVICES];
 int cs_upload_stencil(void) {
-  if (g_stencil_uploaded) return CS_OK;
+  const int dev = cs_device_index();
+  if (g_stencil_uploaded[dev]) return CS_OK;
   int8_t st[14 * 3];
   int n;
   cs_host_canonical_stencil(3, st, &n);
@@ -69,7 +78,7 @@ int cs_upload_stencil(void) {
     h.axis[e] = (int8_t)ax;
   }
   CS_CUDA(cudaMemcpyToSymbol(c_stencil3, &h, sizeof(h)));
-  g_stencil_uploaded = true;
+  g_stencil_uploaded[dev] = true;
   return CS_OK;
 }
 

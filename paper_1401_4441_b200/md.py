@@ -358,6 +358,9 @@ class LJSystem:
         for k, arr in zip(("x", "y", "z", "vx", "vy", "vz"), (x, y, z, vx, vy, vz)):
             b[k][: self.n].copy_(torch.as_tensor(arr, dtype=torch.float64), non_blocking=True)
         b["id"][: self.n].copy_(torch.as_tensor(ids, dtype=torch.int32), non_blocking=True)
+        if not self.verlet:  # (the Verlet rebuild wraps first itself)
+            _lib.call("cs_wrap_positions", self.n, C.byref(self._cbox), _lib.ptr(b["x"]), _lib.ptr(b["y"]),
+                      _lib.ptr(b["z"]), self._s())
         self.rebuild()
 
     def rebuild(self, energy: bool = True):
@@ -403,9 +406,9 @@ class LJSystem:
         """K2 (forces must be zero on entry; build_cells zeroes them)."""
         b = self._buf[self.cur]
         if energy:
-            self.scal[0:1].zero_()
+            _lib.call("cs_memset_async", _lib.ptr(self.scal), 0, 8, self._s())
         if count_pairs:
-            self.npairs.zero_()
+            _lib.call("cs_memset_async", _lib.ptr(self.npairs), 0, 8, self._s())
         if self.verlet:
             _lib.call("cs_lj_forces_verlet", C.byref(self._cbox), C.byref(self._clj),
                       SCHEDULES[self.schedule], self.n, _lib.ptr(self.cell_start), _lib.ptr(self.vlist),
@@ -445,7 +448,7 @@ class LJSystem:
                 self._rebuild_list()
             _lib.call("cs_capture_if_end", side.cuda_stream)
         elif int(self.vflag.item()):
-            self.vflag.zero_()
+            _lib.call("cs_memset_async", _lib.ptr(self.vflag), 0, 4, self._s())
             self._rebuild_list()
 
     def step(self, energy: bool = False):
@@ -624,6 +627,14 @@ class LJSystem:
         return out
 
     # -------------------------------------------------------------- output
+    def bin_errors(self) -> int:
+        """1 if the last cell-list build clamped a particle outside the box
+        into an edge cell (cs_bin_errors; synchronises)."""
+        flag = C.c_int(0)
+        _lib.call("cs_bin_errors", self.n, C.byref(self._cbox), _lib.ptr(self._ws), self._wsb,
+                  C.byref(flag), self._s())
+        return int(flag.value)
+
     def check_status(self):
         """Raise if a kernel reported a capacity overflow (buffered schedule)."""
         st = int(self.status.item())
@@ -680,7 +691,7 @@ def build_cell_list(system: LJSystem) -> None:
 def lj_forces(system: LJSystem, energy: bool = True):
     """Zero the forces, evaluate them; returns (PE, pairs within rc)."""
     for k in ("fx", "fy", "fz"):
-        system._a(k).zero_()
+        _lib.call("cs_memset_async", _lib.ptr(system._a(k)), 0, 8 * system.n, system._s())
     system.compute_forces(energy=energy)
     return system.energies()[0], system.pair_count()
 

@@ -398,7 +398,7 @@ class CudaSlabEngine:
     def take_flag(self) -> int:
         """Verlet mode: this rank's displacement flag (cleared)."""
         v = int(self.vflag.item())
-        self.vflag.zero_()
+        _lib.call("cs_memset_async", _lib.ptr(self.vflag), 0, 4, self._s())
         return v
 
     def wrap(self):
@@ -508,8 +508,8 @@ class CudaSlabEngine:
         """Local forces.  sync=False (Verlet, between rebuilds, no energy): no
         host reads; pairs go to the device accumulator only."""
         a = self.A
-        self.scal[0:1].zero_()
-        self.npairs.zero_()
+        _lib.call("cs_memset_async", _lib.ptr(self.scal), 0, 8, self._s())
+        _lib.call("cs_memset_async", _lib.ptr(self.npairs), 0, 8, self._s())
         if self.verlet:
             _lib.call("cs_lj_forces_verlet", C.byref(self.cbox), C.byref(self.clj), self.sched,
                       self.n_owned + self.n_ghost, _lib.ptr(self.cell_start), _lib.ptr(self.vlist),
