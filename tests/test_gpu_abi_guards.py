@@ -16,12 +16,17 @@ pytestmark = pytest.mark.gpu
 
 
 def test_loopex_rejects_odd_periodic_extent(cuda):
-    box, nuc, a = md.fcc_box((5, 6, 6), 0.8442)  # x: 3 cells (odd), y, z: 4
-    s = md.LJSystem(box, 4 * 5 * 36, schedule="buffered")
-    s.seed_fcc(nuc, a, 0.722, 0.05, 42)
+    """A direct C-ABI caller with an odd periodic extent gets EINVAL (the
+    check runs before any launch, so the buffers are never touched)."""
+    s = md.LJSystem.fcc(6, schedule="loopex")
+    odd = _lib.CsBox()
+    C.memmove(C.byref(odd), C.byref(s._cbox), C.sizeof(odd))
+    odd.nc[1] = odd.gnc[1] = 3
+    odd.L[1] = 3 * 2.6
+    odd.inv[1] = 3 / odd.L[1]
     b = s._buf[s.cur]
     with pytest.raises(ValueError, match="even periodic extents"):
-        _lib.call("cs_lj_forces", C.byref(s._cbox), C.byref(s._clj), _lib.SCHED_LOOPEX, s.n,
+        _lib.call("cs_lj_forces", C.byref(odd), C.byref(s._clj), _lib.SCHED_LOOPEX, s.n,
                   _lib.ptr(s.cell_start), _lib.ptr(b["x"]), _lib.ptr(b["y"]), _lib.ptr(b["z"]),
                   _lib.ptr(b["fx"]), _lib.ptr(b["fy"]), _lib.ptr(b["fz"]), None, None,
                   _lib.ptr(s.status), _lib.ptr(s._ws), s._wsb, s._s())
