@@ -11,8 +11,9 @@ the buffered block schedule, kick.  The link-cell kernel (32^3 cells, rebin
 every step) is measured on the same workload and reported alongside.
 `value` = pair interactions per second (pairs within rc per step x steps/s),
 device-timed with CUDA events per step, L2 flushed between steps.
-N > 1 (torchrun): each rank advances its own cfg2-sized block of a
-weak-scaled system ("scaling": "weak"); see DESIGN.md section on multi-GPU.
+N > 1 (torchrun): each rank advances its own 96^3 FCC block (BASELINE's
+weak-scaling config cfg3) of an x-slab-decomposed system ("scaling": "weak");
+--config cfg4 runs the strong-scaling config; see DESIGN.md section 7.
 `--impl reference` times the CPU port of the reference's own colour-order
 execution (oracle/, OpenMP over all host cores) on the same config.
 """
@@ -277,7 +278,7 @@ def run_reference(args):
                        f"is per pair, sampled on one block" if ws > 1 else ""),
                    "schedule": "loop-exchange colour order, 27 levels, OpenMP over tasks of a level",
                    "steps_per_s": args.steps / tot},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "port",
                          "sample": f"{args.steps} whole {args.config} VV steps (oracle/cs_oracle.c o_md_steps)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -304,10 +305,12 @@ def fp64_peak(torch, lib):
 
 
 def run_slab(args, rank, ws):
-    """N > 1: x-slab decomposition, halos/migration over NCCL.  cfg2 (the
-    default): weak scaling, each rank owns a cfg2-sized slab (28 of 28N
-    Verlet cell planes, 442,368 particles per GPU).  cfg3 / cfg4 / cfg5:
-    strong scaling, the configuration's box cut into N x-slabs."""
+    """N > 1: x-slab decomposition, halos/migration over NCCL.  Default
+    (--config cfg2 not given explicitly): BASELINE's weak-scaling config cfg3
+    with one 96^3 FCC block (3,538,944 particles) per GPU along x -- the N = 1
+    point of that curve is the `configs.cfg3` entry of the one-GPU line.
+    --config cfg3 / cfg4 / cfg5: strong scaling, that configuration's box cut
+    into N x-slabs (cfg4 = BASELINE's strong-scaling config)."""
     import torch
 
     from paper_1401_4441_b200 import _lib, md, slab
@@ -317,13 +320,14 @@ def run_slab(args, rank, ws):
     if verlet:
         args.schedule = "verlet"  # buffered block schedule on the rank-local grid
     weak = args.config == "cfg2"
+    wk = FCC_CONFIGS["cfg3"] if (weak and not args.slab) else NUC  # per-GPU block edge (unit cells)
     # global initial state (same on every rank), built by the single-domain system
     if args.config == "cfg5":
         g = md.LJSystem.liquid_vapour(schedule="buffered", seed=42)
         box, n = g.box, g.n
         nuc = None
     else:
-        nuc = (NUC * ws, NUC, NUC) if weak else (FCC_CONFIGS[args.config],) * 3
+        nuc = (wk * ws, wk, wk) if weak else (FCC_CONFIGS[args.config],) * 3
         box, nucs, a = md.fcc_box(nuc, 0.8442)
         n = 4 * nucs[0] * nucs[1] * nucs[2]
         g = md.LJSystem(box, n, schedule="loopex")
@@ -393,10 +397,12 @@ def run_slab(args, rank, ws):
     clocks = clk.summary()
     if rank != 0:
         return
-    workload = (f"cfg2 per GPU, x-slab weak scaling: FCC {nuc[0]}x48x48 = {n} particles, " if weak else
+    workload = (f"{'cfg3' if wk != NUC else 'cfg2'} block per GPU, x-slab weak scaling: FCC {nuc[0]}x{wk}x{wk} "
+                f"= {n} particles, " if weak else
                 f"{args.config} ({n} particles) cut into {ws} x-slabs (strong scaling): ")
     line = {
-        "metric": METRIC if weak else metric_of(args.config), "value": pairs / tot_s, "unit": UNIT,
+        "metric": (metric_of("cfg3") + " per GPU, weak scaling" if weak and wk != NUC else
+                   METRIC if weak else metric_of(args.config)), "value": pairs / tot_s, "unit": UNIT,
         "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True,
         "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
@@ -420,17 +426,18 @@ def run_slab(args, rank, ws):
     print(json.dumps(line), flush=True)
 
 
-def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True):
+def measure(torch, md, schedule, args, steps, rank, ws, dev, clocks=True, config=None):
     """Timed run: `steps` VV steps, each replayed as ONE CUDA graph (the
     production path, LJSystem.graph_step), device-timed with CUDA events, L2
     flushed before every step.  Breakdown run: up to 30 more steps replayed as
     three graphs (pre | force | post) with events between the phases, for the
     force-kernel time and the roofline.  Per-step counts stay on the device
     (no host synchronisation inside either loop)."""
-    if args.config == "cfg5":
+    config = config or args.config
+    if config == "cfg5":
         sysm = md.LJSystem.liquid_vapour(schedule=schedule, block=args.block, seed=42 + rank, skin=args.skin)
     else:
-        sysm = md.LJSystem.fcc(FCC_CONFIGS[args.config], schedule=schedule, block=args.block, seed=42 + rank,
+        sysm = md.LJSystem.fcc(FCC_CONFIGS[config], schedule=schedule, block=args.block, seed=42 + rank,
                                skin=args.skin)
     pre, force, post = sysm.graph_phases()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
@@ -523,13 +530,39 @@ def run_ours(args):
               "roofline_frac": ml["achieved"] / peak_fp64, "steps": len(ml["step_ms"])}
         del ml
     e2e = e2e_run(torch, md, sysm, args)
+    colour = None
+    if ws == 1 and args.config == "cfg2" and not args.no_variants:
+        # the north star's conflict-free colour-ordered schedules on the same
+        # workload, each with its own roofline
+        colour = {}
+        for sched in ("verlet_dataflow", "verlet_shell", "loopex"):
+            mv = measure(torch, md, sched, args, min(args.steps, 20), rank, ws, dev, clocks=False)
+            colour[sched] = point_summary(mv, peak_fp64)
+            colour[sched]["schedule"] = COLOUR_LABELS[sched]
+            del mv
+            torch.cuda.empty_cache()
+    configs = None
+    if ws == 1 and args.config == "cfg2" and not args.no_configs:
+        # the 1-GPU points of BASELINE's other configurations (cfg3 = the
+        # weak-scaling block, cfg4 = the largest single-GPU config, cfg5 = the
+        # load-imbalance stress), each with roofline, e2e and clocks
+        configs = {}
+        for cname, nsteps in (("cfg3", 20), ("cfg4", 10), ("cfg5", 20)):
+            mc = measure(torch, md, args.schedule, args, nsteps, rank, ws, dev, config=cname)
+            row = point_summary(mc, peak_fp64)
+            row.update({"metric": metric_of(cname), "workload": workload_of(cname), "particles": mc["sys"].n,
+                        "cells": list(mc["sys"].box.cells), "e2e": e2e_run(torch, md, mc["sys"], args, nsteps),
+                        "clocks": mc["clocks"]})
+            configs[cname] = row
+            del mc
+            torch.cuda.empty_cache()
     if rank != 0:
         return
     cpu = None
     if ws == 1 and not args.no_cpu:
         cores = len(os.sched_getaffinity(0))
         v, nst, el = cpu_sample(cores, min_seconds=args.cpu_seconds, config=args.config)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "port",
                "sample": f"{nst} whole {args.config} VV steps in {el:.1f} s (oracle o_md_steps, loop-exchange colour order on OpenMP threads)"}
         if args.config in FCC_CONFIGS and args.config != "cfg4":
             v1, el1 = cpu_task_replay(args.config)
@@ -588,9 +621,50 @@ def run_ours(args):
                         + (m["builds"] or 0) * getattr(sysm, "REBUILD_LAUNCHES", 0),
         "clocks": m["clocks"],
     }
+    if colour:
+        line["colour_ordered"] = colour
+    if configs:
+        line["configs"] = configs
     if ws == 1 and args.config == "cfg2" and not args.no_schedule:
         line["schedule_analysis"] = schedule_report(torch, cpu=not args.no_cpu)
     print(json.dumps(line), flush=True)
+
+
+COLOUR_LABELS = {
+    "verlet_dataflow": "Verlet round tables, 2x2x2 block colour order executed as a dataflow (one persistent "
+                       "launch; a block waits only for its lower-colour neighbours), 28^3 cells",
+    "verlet_shell": "Verlet round tables, 8 colour passes of 2x2x2 blocks (global barrier per colour), 28^3 cells",
+    "loopex": "link cells (32^3), the reference's loop-exchange colour order as 27 passes (generate_loopex "
+              "levels, one warp per cell-pair task), rebinned every step",
+}
+
+
+def point_summary(m, peak_fp64):
+    """Compact record of one measure() run: throughput, step/force time and
+    the force kernel's FP64 roofline under both C conventions."""
+    sysm = m["sys"]
+    return {"value": m["value"], "unit": UNIT, "steps": len(m["step_ms"]),
+            "ms_per_step": 1e3 * m["tot_s"] / len(m["step_ms"]),
+            "force_ms_per_step": statistics.mean(m["force_ms"]),
+            "pairs_per_step": statistics.mean(m["pairs"]),
+            "candidates_tested_per_step": statistics.mean(m["cands"]),
+            "list_rebuilds_in_timed_steps": m["builds"],
+            "roofline": {"bound": "fp64", "unit": "TFLOP/s", "peak": peak_fp64,
+                         "achieved": m["achieved"], "frac": m["achieved"] / peak_fp64,
+                         "achieved_tested": m["achieved_tested"],
+                         "frac_tested": m["achieved_tested"] / peak_fp64},
+            "skin": sysm.skin if sysm.verlet else None}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def hbm_side(sysm, force_ms, schedule):
@@ -661,6 +735,81 @@ def schedule_report(torch, cpu=True):
     out["note"] = ("device: stream generation + edge detection + critical path (wall clock incl. "
                    "allocations); cpu_port: oracle/cs_oracle.c restatement of the same pipeline, 1 core")
     out["payload"] = payload_report(torch, cpu)
+    if cpu:
+        try:
+            out["reference_python"] = reference_python_report(torch)
+        except Exception as exc:  # the reference arm must not sink the bench line
+            out["reference_python"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
+    return out
+
+
+def reference_python_report(torch):
+    """the UNMODIFIED reference package, installed
+    into baseline/_ref (pip, from a copy of /root/reference/pkg), timed on the
+    box's host: generate -> detect_dependencies -> critical_path
+    (taskgen.py:180-234, depgraph.py:102-174) on the cfg1 grid and on 32^3,
+    and executor.execute (executor.py:287-354) with W = all host cores on the
+    colour-order stream with the integer payload; beside each, the same
+    pipeline / execution on the device."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "cellsched")):
+        return {"unavailable": "baseline/_ref not installed (pip install of /root/reference/pkg)"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import cellsched as R
+    from cellsched import executor as RX
+
+    from paper_1401_4441_b200 import GridSpec, generic, schedule, taskgen
+
+    cores = len(os.sched_getaffinity(0))
+    out = {"package": f"cellsched {R.__version__} (baseline/_ref)", "cores": cores, "cpu_model": cpu_model(),
+           "pipeline": {}, "executor": {}}
+    for gname, ext in (("cfg1", (4, 4, 4)), ("32^3", (32, 32, 32))):
+        g = R.GridSpec(ext)
+        rows = {}
+        for label, strat in (("lexicographic", "basic"), ("colour 2x2x2", "loopex")):
+            t0 = time.perf_counter()
+            tasks = (R.generate_basic(g, R.StencilOrder.canonical(3)) if strat == "basic"
+                     else R.generate_loopex(g))
+            t1 = time.perf_counter()
+            graph = R.detect_dependencies(tasks)
+            t2 = time.perf_counter()
+            depth = R.critical_path(graph)
+            t3 = time.perf_counter()
+            schedule.device_stream(GridSpec(ext), strat).depth()  # warm-up
+            torch.cuda.synchronize()
+            d0 = time.perf_counter()
+            ds = schedule.device_stream(GridSpec(ext), strat)
+            ds.edges()
+            ddev = ds.depth()
+            torch.cuda.synchronize()
+            d1 = time.perf_counter()
+            rows[label] = {"tasks": len(tasks), "depth": depth, "generate_s": t1 - t0, "detect_s": t2 - t1,
+                           "critical_path_s": t3 - t2, "total_s": t3 - t0, "device_ms": 1e3 * (d1 - d0),
+                           "device_depth": ddev, "speedup": (t3 - t0) / (d1 - d0)}
+            del tasks, graph, ds
+        out["pipeline"][gname] = rows
+    for gname, ext in (("cfg1", (4, 4, 4)), ("16^3", (16, 16, 16))):
+        g = R.GridSpec(ext)
+        graph = R.detect_dependencies(R.generate_loopex(g))
+        res = RX.execute(graph, RX.ExecConfig(cores, 0, payload_seed=42), g)
+        mine = taskgen.generate_loopex(GridSpec(ext))
+        generic.execute_dag(mine, GridSpec(ext), 42)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        acc, conflicts = generic.execute_dag(mine, GridSpec(ext), 42)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out["executor"][gname] = {
+            "tasks": graph.task_count, "threads": cores, "wall_s": res.wall_ns * 1e-9,
+            "tasks_per_s": graph.task_count / (res.wall_ns * 1e-9),
+            "device_dag_execute_s": dt, "device_tasks_per_s": graph.task_count / dt,
+            "device_note": "wall clock incl. host interning of the Task objects and edge detection",
+            "device_conflicts": conflicts,
+            "accumulators_equal": res.accumulators == acc}
+    out["note"] = ("reference Python, single process (the executor's worker threads share the GIL); "
+                   "device = this package's stream generator + detector + depth (wall clock incl. allocations) "
+                   "and its ready-queue DAG runtime (cs_dag_execute) with the same payload")
     return out
 
 
@@ -709,11 +858,12 @@ def payload_report(torch, cpu=True, ext=(64, 64, 192), seed=42):
     return row
 
 
-def e2e_run(torch, md, ref_sys, args):
+def e2e_run(torch, md, ref_sys, args, steps=None):
     """Same metric through the public API from pinned host buffers: upload the
     state, K graph-replayed steps each reading back (PE, KE), download the
     final state -- all inside the timed region."""
     n = ref_sys.n
+    steps = steps or args.steps
     host = {k: v[:n].cpu().pin_memory() for k, v in ref_sys.initial.items()}
     sysm = md.LJSystem(ref_sys.box, n, schedule=ref_sys.schedule, block=ref_sys.block, skin=ref_sys.skin)
     sysm.load_host(host["x"], host["y"], host["z"], host["vx"], host["vy"], host["vz"], host["id"])
@@ -724,9 +874,9 @@ def e2e_run(torch, md, ref_sys, args):
     t0 = time.perf_counter()
     sysm.load_host(host["x"], host["y"], host["z"], host["vx"], host["vy"], host["vz"], host["id"])
     pairs = 0
-    res = torch.zeros(args.steps, dtype=torch.int64).pin_memory()
-    for k in range(args.steps):
-        sysm.graph_step(energy=k == args.steps - 1)  # the last step also reports the energies
+    res = torch.zeros(steps, dtype=torch.int64).pin_memory()
+    for k in range(steps):
+        sysm.graph_step(energy=k == steps - 1)  # the last step also reports the energies
         # the step's result (its pair count, the metric) goes to the host every
         # step, asynchronously into its own pinned slot: the host never waits
         res[k].copy_(sysm.npairs[0], non_blocking=True)
@@ -738,9 +888,9 @@ def e2e_run(torch, md, ref_sys, args):
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     h2d = 52 * n
-    d2h = 8 * args.steps + 80 + 48 * n
-    return {"value": pairs / el, "unit": UNIT, "h2d_bytes_per_step": h2d / args.steps,
-            "d2h_bytes_per_step": d2h / args.steps,
+    d2h = 8 * steps + 80 + 48 * n
+    return {"value": pairs / el, "unit": UNIT, "h2d_bytes_per_step": h2d / steps,
+            "d2h_bytes_per_step": d2h / steps,
             "timed": ("host wall clock: H2D of the initial state (incl. its cell list, Verlet list and "
                       "forces), K graph-replayed steps each copying its pair count to pinned host memory "
                       "(async D2H per step), the last one with energies read back, D2H of the final state")}
@@ -762,6 +912,8 @@ def main():
     ap.add_argument("--skin", type=float, default=0.35, help="Verlet skin (verlet schedules)")
     ap.add_argument("--block", type=lambda s: tuple(int(v) for v in s.split(",")), default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the colour-ordered schedule runs")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg3/cfg4/cfg5 one-GPU points")
     ap.add_argument("--no-schedule", action="store_true", help="skip the cfg1/cfg5 serialization analysis")
     ap.add_argument("--slab", action="store_true", help="use the x-slab engine even at N=1")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -60,6 +60,14 @@ __device__ __forceinline__ double wrap_dev(double x, double L) {
   return x;
 }
 
+// any distance from the box (host-loaded positions): one floor reduction when
+// more than a box length outside, then the single-step wrap -- identical to
+// wrap_dev for positions within one box length of [0, L)
+__device__ __forceinline__ double wrap_far(double x, double L) {
+  if (x < -L || x >= 2.0 * L) x = __dadd_rn(x, -__dmul_rn(L, floor(x / L)));
+  return wrap_dev(wrap_dev(x, L), L);
+}
+
 // ------------------------------------------------------------------ setup --
 struct FccArgs {
   int nuc[3];

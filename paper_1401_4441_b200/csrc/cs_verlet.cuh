@@ -508,9 +508,9 @@ __global__ void k_wrap_copy(int64_t n, double Lx, double Ly, double Lz, double *
                             double *z) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] = wrap_dev(x[i], Lx);
-    y[i] = wrap_dev(y[i], Ly);
-    z[i] = wrap_dev(z[i], Lz);
+    x[i] = wrap_far(x[i], Lx);
+    y[i] = wrap_far(y[i], Ly);
+    z[i] = wrap_far(z[i], Lz);
   }
 }
 

@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT
 make -s -C oracle
-timeout 1500 python -m pytest tests/test_gpu_schedsim.py tests/test_gpu_fullsize.py -q -p no:cacheprovider -s --durations=20 > gpurun_out/rq_tests.log 2>&1; echo rc=$? >> gpurun_out/rq_tests.log
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x --durations=15 > gpurun_out/r2_tests.log 2>&1; echo rc=$? >> gpurun_out/r2_tests.log
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err; echo rc=$? >> gpurun_out/r2_bench.err
