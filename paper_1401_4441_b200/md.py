@@ -246,6 +246,8 @@ class LJSystem:
         self.status = self._out[72:76].view(torch.int32)  # kernel capacity flags
         self._out_host = torch.empty(80, dtype=torch.uint8).pin_memory()
         self.dt = 0.005
+        self.nstep = 0  # VV steps taken (eager or replayed); kept in checkpoints
+        self.seed = None
         self._graphs = {}
         self._capturing = False
         if self.verlet:
@@ -326,6 +328,7 @@ class LJSystem:
     def seed_positions(self, xyz, temperature, seed):
         """Host positions (ids = row order) + device Gaussian velocities at T."""
         torch = _torch()
+        self.seed = int(seed)
         b = self._buf[self.cur]
         for k, col in zip(("x", "y", "z"), range(3)):
             b[k][: self.n].copy_(torch.as_tensor(xyz[:, col], dtype=torch.float64))
@@ -337,6 +340,7 @@ class LJSystem:
         self.rebuild()
 
     def seed_fcc(self, nuc, a, temperature, jitter, seed):
+        self.seed = int(seed)
         src = self.cur
         b = self._buf[src]
         nu = (C.c_int32 * 3)(*nuc)
@@ -453,6 +457,8 @@ class LJSystem:
 
     def step(self, energy: bool = False):
         """One velocity-Verlet step (K3 kick+drift, K1, K2, K3 kick)."""
+        if not self._capturing:
+            self.nstep += 1
         hdtm = 0.5 * self.dt / self.params.mass
         if self.verlet:
             self._pre_verlet()
@@ -505,6 +511,7 @@ class LJSystem:
     def graph_step(self, energy: bool = False):
         """One VV step replayed from a CUDA graph (one graph per parity)."""
         self._graph(("step", energy), lambda: self.step(energy))
+        self.nstep += 1
 
     def graph_phases(self):
         """The step as three graphs (kick+drift+rebin | forces | kick), so a
@@ -625,6 +632,62 @@ class LJSystem:
                 pe, ke = self.energies()
                 out.append((k, pe, ke))
         return out
+
+    # --------------------------------------------------- checkpoint/resume
+    _STATE = ("x", "y", "z", "vx", "vy", "vz", "fx", "fy", "fz", "id")
+
+    def checkpoint(self, path) -> None:
+        """npz of the full step state: positions, velocities, forces and ids in
+        cell order, the cell list, step counter, seed, box, parameters and
+        schedule; Verlet systems also store the reference positions, the
+        round tables and the displacement flag, so `restore` continues
+        bit-identically (no list rebuild at load)."""
+        import numpy as np
+
+        torch = _torch()
+        torch.cuda.current_stream().synchronize()
+        b = self._buf[self.cur]
+        n = self.n
+        d = {k: b[k][:n].cpu().numpy() for k in self._STATE}
+        d.update(cell_start=self.cell_start.cpu().numpy(), nstep=self.nstep,
+                 seed=-1 if self.seed is None else self.seed, lengths=np.asarray(self.box.lengths),
+                 cells=np.asarray(self.box.cells), block=np.asarray(self.block), dt=self.dt,
+                 skin=self.skin, schedule=self.schedule,
+                 params=np.asarray([self.params.epsilon, self.params.sigma, self.params.rc, self.params.mass]))
+        if self.verlet:
+            d.update(xref=np.stack([t[:n].cpu().numpy() for t in self.xref]), vlist=self.vlist.cpu().numpy(),
+                     vflag=self.vflag.cpu().numpy(), graph_builds=self.graph_builds.cpu().numpy(),
+                     list_builds=self.list_builds)
+        np.savez(path, **d)
+
+    @classmethod
+    def restore(cls, path, device=None) -> "LJSystem":
+        """A system continuing exactly from `checkpoint(path)`."""
+        import numpy as np
+
+        torch = _torch()
+        z = np.load(path)
+        eps, sig, rc, mass = (float(v) for v in z["params"])
+        box = LJBox(tuple(float(v) for v in z["lengths"]), tuple(int(v) for v in z["cells"]))
+        n = int(len(z["x"]))
+        s = cls(box, n, LJParams(eps, sig, rc, mass), str(z["schedule"]),
+                tuple(int(v) for v in z["block"]), device=device, skin=float(z["skin"]))
+        s.dt = float(z["dt"])
+        s.nstep = int(z["nstep"])
+        s.seed = None if int(z["seed"]) < 0 else int(z["seed"])
+        b = s._buf[s.cur]
+        for k in cls._STATE:
+            b[k][:n].copy_(torch.from_numpy(z[k]))
+        s.cell_start.copy_(torch.from_numpy(z["cell_start"]))
+        if s.verlet:
+            for t, a in zip(s.xref, z["xref"]):
+                t[:n].copy_(torch.from_numpy(a))
+            s.vlist.copy_(torch.from_numpy(z["vlist"]))
+            s.vflag.copy_(torch.from_numpy(z["vflag"]))
+            s.graph_builds.copy_(torch.from_numpy(z["graph_builds"]))
+            s.list_builds = int(z["list_builds"])
+        s.initial = {k: b[k].clone() for k in ("x", "y", "z", "vx", "vy", "vz", "id")}
+        return s
 
     # -------------------------------------------------------------- output
     def bin_errors(self) -> int:
