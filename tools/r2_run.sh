@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-make -s -C oracle
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x --durations=15 > gpurun_out/r2_tests.log 2>&1; echo rc=$? >> gpurun_out/r2_tests.log
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err; echo rc=$? >> gpurun_out/r2_bench.err
+timeout 900 python -m pytest tests/test_gpu_checkpoint.py -q -p no:cacheprovider > gpurun_out/r2_tests.log 2>&1; echo rc=$? >> gpurun_out/r2_tests.log
+timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard python tools/racecheck_cfg1.py > gpurun_out/r2_racecheck.log 2>&1; echo rc=$? >> gpurun_out/r2_racecheck.log
