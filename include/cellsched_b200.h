@@ -52,6 +52,10 @@ int cs_device_synchronize(void);
 /* stream-ordered byte fill of device memory (cudaMemsetAsync; a memset node
  * when captured): clears per-step result words without framework kernels */
 int cs_memset_async(void *dst, int value, size_t bytes, void *stream);
+/* stream-ordered device-to-device copy (a memcpy node when captured) */
+int cs_copy_async(void *dst, const void *src, size_t bytes, void *stream);
+/* *acc += *x on the stream: device-side running totals (pair counts) */
+int cs_accumulate_i64(int64_t *acc, const int64_t *x, void *stream);
 
 /* ===================== K4: task streams and serialization depth ========== */
 enum { CS_STREAM_BASIC = 0, CS_STREAM_LOOPEX = 1 };

@@ -81,6 +81,8 @@ _SIGS = {
     "cs_build_cells": (C.c_int, [_I64, _P] + [_P] * 18 + [_P, _SZ, _P]),
     "cs_bin_errors": (C.c_int, [_I64, _P, _P, _SZ, _P, _P]),
     "cs_memset_async": (C.c_int, [_P, C.c_int, _SZ, _P]),
+    "cs_copy_async": (C.c_int, [_P, _P, _SZ, _P]),
+    "cs_accumulate_i64": (C.c_int, [_P, _P, _P]),
     "cs_force_ws_bytes": (_SZ, [_P, C.c_int, _I64]),
     "cs_lj_forces": (C.c_int, [_P, _P, C.c_int, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "cs_vv_kick_predict": (C.c_int, [_I64, _D, _D, C.c_int] + [_P] * 12 + [_D, _P, _P]),

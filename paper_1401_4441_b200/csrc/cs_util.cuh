@@ -28,6 +28,20 @@ extern "C" int cs_device_synchronize(void) {
   CS_CUDA(cudaDeviceSynchronize());
   return CS_OK;
 }
+// device-to-device copy on the stream (a memcpy node when captured)
+extern "C" int cs_copy_async(void *dst, const void *src, size_t bytes, void *stream) {
+  if (bytes == 0) return CS_OK;
+  CS_REQUIRE(dst && src, "cs_copy_async: null pointer");
+  CS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, cs_stream(stream)));
+  return CS_OK;
+}
+__global__ void k_accumulate_i64(unsigned long long *acc, const unsigned long long *x) { *acc += *x; }
+// *acc += *x on the stream (device-side running totals, no host read)
+extern "C" int cs_accumulate_i64(int64_t *acc, const int64_t *x, void *stream) {
+  k_accumulate_i64<<<1, 1, 0, cs_stream(stream)>>>((unsigned long long *)acc,
+                                                   (const unsigned long long *)x);
+  return cs_check_launch("accumulate_i64");
+}
 // stream-ordered fill (captured as a memset node inside CUDA graphs): the
 // per-step result words are cleared through the C ABI, not by torch kernels
 extern "C" int cs_memset_async(void *dst, int value, size_t bytes, void *stream) {

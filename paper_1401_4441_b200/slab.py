@@ -500,9 +500,9 @@ class CudaSlabEngine:
         """Verlet, between rebuilds: same ghost particles in the same slots --
         overwrite their positions only (no cell-list work, no host sync)."""
         m, o, a = self.n_ghost, self.n_owned, self.A
-        xyz = xyz.view(3, m)
+        src = xyz.view(3, m)
         for k, key in enumerate(("x", "y", "z")):
-            a[key][o:o + m].copy_(xyz[k])
+            _lib.call("cs_copy_async", _lib.ptr(a[key][o:o + m]), _lib.ptr(src[k]), 8 * m, self._s())
 
     def forces(self, energy, sync: bool = True):
         """Local forces.  sync=False (Verlet, between rebuilds, no energy): no
@@ -516,7 +516,7 @@ class CudaSlabEngine:
                       _lib.ptr(a["x"]), _lib.ptr(a["y"]), _lib.ptr(a["z"]), _lib.ptr(a["fx"]),
                       _lib.ptr(a["fy"]), _lib.ptr(a["fz"]), _lib.ptr(self.scal) if energy else None,
                       _lib.ptr(self.npairs), _lib.ptr(self.status), _lib.ptr(self.ws), self.wsb, self._s())
-            self.pairs_acc += self.npairs
+            _lib.call("cs_accumulate_i64", _lib.ptr(self.pairs_acc), _lib.ptr(self.npairs), self._s())
             if not sync:
                 return 0.0, 0
             if int(self.status.item()):
@@ -527,7 +527,7 @@ class CudaSlabEngine:
                   _lib.ptr(a["y"]), _lib.ptr(a["z"]), _lib.ptr(a["fx"]), _lib.ptr(a["fy"]),
                   _lib.ptr(a["fz"]), _lib.ptr(self.scal) if energy else None, _lib.ptr(self.npairs),
                   _lib.ptr(self.status), _lib.ptr(self.ws), self.wsb, self._s())
-        self.pairs_acc += self.npairs
+        _lib.call("cs_accumulate_i64", _lib.ptr(self.pairs_acc), _lib.ptr(self.npairs), self._s())
         if int(self.status.item()):
             raise _lib.CellschedError("force kernel capacity overflow (use schedule='shell')")
         return float(self.scal[0].item()) if energy else 0.0, int(self.npairs.item())
