@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python tools/time_build.py 10 > gpurun_out/r2_build.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:"k_vb_" -c 2 python tools/time_build.py 1 > gpurun_out/r2_ncu_build.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_verlet.py -x -q -p no:cacheprovider > gpurun_out/r2_tests.log 2>&1; echo rc=$? >> gpurun_out/r2_tests.log
+make -s -C oracle
+timeout 1700 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=10 > gpurun_out/r2_tests.log 2>&1; echo rc=$? >> gpurun_out/r2_tests.log
+timeout 600 python __graft_entry__.py smoke > gpurun_out/r2_smoke.log 2>&1; echo rc=$? >> gpurun_out/r2_smoke.log
+timeout 300 python bench.py --slab --steps 30 --warmup 5 --no-cpu > gpurun_out/r2_slab.json 2>&1; echo rc=$? >> gpurun_out/r2_slab.json
