@@ -414,17 +414,58 @@ __device__ __forceinline__ void merge_cell(const ShellArgs &SA, SM &S, int lc, i
   if (g0 < 0) return;
   const int f0 = S.fstart[lc], n = S.fstart[lc + 1] - f0;
   const int nc = S.mt_n[lc];
-  for (int i = lane; i < n; i += 32) {
-    double sx = 0, sy = 0, sz = 0;
-    for (int k = 0; k < nc; ++k) {
-      const int base = S.mt_base[lc][k];
-      if (base < 0) continue;
-      const int s = base + i;
-      sx += S.RF[0][s];
-      sy += S.RF[1][s];
-      sz += S.RF[2][s];
+  if constexpr (MODE == SH_DATAFLOW) {
+    // f of this cell is final for every lower colour (the block waited for
+    // them) and nobody else writes it before this block publishes: its L2
+    // reads go first (two particles per lane), so their latency overlaps
+    // the slot sums instead of following them
+    const ForceArgs &A = SA.A;
+    for (int i0 = 0; i0 < n; i0 += 64) {
+      const int ia = i0 + lane, ib = i0 + 32 + lane;
+      const bool va = ia < n, vb = ib < n;
+      const double ax = va ? __ldcg(A.fx + g0 + ia) : 0.0, ay = va ? __ldcg(A.fy + g0 + ia) : 0.0,
+                   az = va ? __ldcg(A.fz + g0 + ia) : 0.0;
+      const double bx = vb ? __ldcg(A.fx + g0 + ib) : 0.0, by = vb ? __ldcg(A.fy + g0 + ib) : 0.0,
+                   bz = vb ? __ldcg(A.fz + g0 + ib) : 0.0;
+      double sx = 0, sy = 0, sz = 0, tx = 0, ty = 0, tz = 0;
+      for (int k = 0; k < nc; ++k) {
+        const int base = S.mt_base[lc][k];
+        if (base < 0) continue;
+        if (va) {
+          sx += S.RF[0][base + ia];
+          sy += S.RF[1][base + ia];
+          sz += S.RF[2][base + ia];
+        }
+        if (vb) {
+          tx += S.RF[0][base + ib];
+          ty += S.RF[1][base + ib];
+          tz += S.RF[2][base + ib];
+        }
+      }
+      if (va) {
+        A.fx[g0 + ia] = ax + sx;
+        A.fy[g0 + ia] = ay + sy;
+        A.fz[g0 + ia] = az + sz;
+      }
+      if (vb) {
+        A.fx[g0 + ib] = bx + tx;
+        A.fy[g0 + ib] = by + ty;
+        A.fz[g0 + ib] = bz + tz;
+      }
     }
-    merge_store<MODE>(SA, boff + f0 + i, g0 + i, sx, sy, sz);
+  } else {
+    for (int i = lane; i < n; i += 32) {
+      double sx = 0, sy = 0, sz = 0;
+      for (int k = 0; k < nc; ++k) {
+        const int base = S.mt_base[lc][k];
+        if (base < 0) continue;
+        const int s = base + i;
+        sx += S.RF[0][s];
+        sy += S.RF[1][s];
+        sz += S.RF[2][s];
+      }
+      merge_store<MODE>(SA, boff + f0 + i, g0 + i, sx, sy, sz);
+    }
   }
 }
 
