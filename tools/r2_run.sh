@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-for s in verlet_dataflow verlet dataflow; do timeout 200 python tools/time_force.py $s 50; done > gpurun_out/r2_force.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_verlet.py tests/test_gpu_lj.py tests/test_gpu_edges.py -x -q -p no:cacheprovider > gpurun_out/r2_tests.log 2>&1; echo rc=$? >> gpurun_out/r2_tests.log
+timeout 300 python tools/e2e_breakdown.py 20 > gpurun_out/r2_e2e.log 2>&1
