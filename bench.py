@@ -67,9 +67,9 @@ def workload_of(config):
 
 def ncu_fp64_pipe(schedule):
     """FP64 pipe activity (% of peak, ncu) of the schedule's force kernel, from
-    the committed capture (profiles/r01_traffic.json), or None."""
+    the committed capture (profiles/r02_traffic.json), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             t = json.load(f)
         return t["kernels"]["verlet" if schedule.startswith("verlet") else "buffered"].get("fp64_pipe_active_pct")
     except (OSError, KeyError, ValueError):
@@ -78,9 +78,9 @@ def ncu_fp64_pipe(schedule):
 
 def traffic_bytes(schedule):
     """DRAM bytes per force launch of the schedule's kernel, from the committed
-    ncu --set full capture (profiles/r01_traffic.json)."""
+    ncu --set full capture (profiles/r02_traffic.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             t = json.load(f)
         return t.get("per_schedule", {}).get(schedule, t.get("dram_bytes_per_launch") if schedule == "buffered" else None)
     except (OSError, KeyError, ValueError):
