@@ -70,6 +70,10 @@ struct ShellBase {
   int overflow;
   uint8_t mt_n[SH_MAXF];           // merge-table counts in shared memory (lanes of one warp
                                    //   read different cells: divergent constant reads serialise)
+  // Verlet dataflow: the lower-colour neighbour blocks this block's merges
+  // must follow (flag indices, -1 = none) and whether they have published
+  int dep[27];
+  int depok;
 };
 struct ShellSmem : ShellBase<SH_RCAP, SH_HCAP, 1> {  // link-cell super-tasks
   double rows[SH_NW][SH_IB][3][32];  // per-lane i partials
@@ -480,6 +484,20 @@ __device__ __forceinline__ void verlet_merge_queue(const ShellArgs &SA, SM &S, i
     if (lane == 0) t = atomicAdd(&S.qhead, 1);
     t = __shfl_sync(CS_FULL, t, 0);
     if (t >= nfc) break;
+    if constexpr (MODE == SH_DATAFLOW) {
+      // the colour order binds only the updates of f: the block computed its
+      // rounds without waiting, and merges after its lower-colour neighbour
+      // blocks have published theirs
+      if (!*(volatile int *)&S.depok) {
+        if (lane < 27 && S.dep[lane] >= 0) {
+          const volatile int *f = SA.flags + S.dep[lane];
+          while (*f == 0) __nanosleep(64);
+        }
+        __syncwarp();
+        __threadfence();
+        if (lane == 0) *(volatile int *)&S.depok = 1;
+      }
+    }
     int lc = -1;
     if (lane == 0) {
       volatile int *qv = S.queue;
@@ -966,7 +984,31 @@ __global__ void __launch_bounds__(SH_NW * 32, VERLET ? 2 : 3) k_force_shell(Shel
       const int cnt0 = (A.nbk[0] - kc[0] + 1) >> 1, cnt1 = (A.nbk[1] - kc[1] + 1) >> 1;
       const int kb[3] = {2 * (idx % cnt0) + kc[0], 2 * ((idx / cnt0) % cnt1) + kc[1],
                          2 * (idx / (cnt0 * cnt1)) + kc[2]};
-      if (threadIdx.x < 27 && threadIdx.x != 13) {
+      if (VERLET) {
+        // record the lower-colour neighbours; the wait happens before the
+        // block's first footprint merge (verlet_merge_queue), not here
+        ShellSmemVL &S = *reinterpret_cast<ShellSmemVL *>(sh_raw);
+        if (threadIdx.x < 27) {
+          int dep = -1;
+          if (threadIdx.x != 13) {
+            const int d[3] = {(int)threadIdx.x % 3 - 1, ((int)threadIdx.x / 3) % 3 - 1,
+                              (int)threadIdx.x / 9 - 1};
+            int nbc[3];
+            bool ok = true;
+            for (int k = 0; k < 3; ++k) {
+              nbc[k] = kb[k] + d[k];
+              if (nbc[k] < 0 || nbc[k] >= A.nbk[k]) {
+                if (A.b.per[k]) nbc[k] = wrap1i(nbc[k], A.nbk[k]);
+                else ok = false;
+              }
+            }
+            const int ncol = (nbc[0] & 1) | ((nbc[1] & 1) << 1) | ((nbc[2] & 1) << 2);
+            if (ok && ncol < c) dep = nbc[0] + A.nbk[0] * (nbc[1] + A.nbk[1] * nbc[2]);
+          }
+          S.dep[threadIdx.x] = dep;
+        }
+        if (threadIdx.x == 0) S.depok = 0;
+      } else if (threadIdx.x < 27 && threadIdx.x != 13) {
         const int d[3] = {(int)threadIdx.x % 3 - 1, ((int)threadIdx.x / 3) % 3 - 1, (int)threadIdx.x / 9 - 1};
         int nbc[3];
         bool ok = true;
