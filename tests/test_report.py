@@ -47,3 +47,21 @@ def test_device_depth_rows(cuda):
     assert basic[cols.index("makespan")] == "692" and loopex[cols.index("makespan")] == "27"
     assert basic[cols.index("tasks")] == loopex[cols.index("tasks")] == str(14 * 64)
     assert basic[cols.index("kind")] == "device" and int(loopex[cols.index("duration_ns")]) > 0
+
+
+def test_simulated_row_and_row_records(tmp_path):
+    class Res:  # the SimResult fields simulated_row reads
+        workers, serial_time, makespan = 8, 42000, 5261
+        speedup = 42000 / 5261
+        utilization = 42000 / (8 * 5261)
+
+    g = GridSpec((30, 10, 10))
+    row = report.simulated_row(Res(), "basic", g, order=StencilOrder.canonical(3), delta=10)
+    cols = report.CSV_COLUMNS
+    assert row[cols.index("kind")] == "simulated" and row[cols.index("order")] == "canonical"
+    assert row[cols.index("makespan")] == "5261" and row[cols.index("speedup")] == "7.983273"
+    assert row[cols.index("utilization")] == "0.997909" and row[cols.index("ez")] == "10"
+    rec = report.Row("device", "loopex", 3, 4, 4, 4, tasks=896, makespan=27)
+    p = report.write_csv(tmp_path / "r.csv", [rec, row])
+    lines = p.read_text().splitlines()
+    assert lines[1] == "device,loopex,3,4,4,4,,,,896,27,,,," and len(lines) == 3
