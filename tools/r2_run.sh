@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 python tools/prof_force.py verlet_dataflow > gpurun_out/r2_forcedf_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_force_shell -s 1 -c 1 \
-  -o gpurun_out/r2_forcedf3_full python tools/prof_force.py verlet_dataflow > gpurun_out/r2_forcedf3_full.log 2>&1
+make -s -C oracle
+timeout 200 python tools/time_build.py 10 > gpurun_out/r2_build.log 2>&1
+timeout 200 python tools/time_force.py verlet 30 >> gpurun_out/r2_build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_verlet.py tests/test_gpu_fullsize.py tests/test_gpu_cfg5.py tests/test_gpu_checkpoint.py -x -q -p no:cacheprovider > gpurun_out/r2_tests.log 2>&1; echo rc=$? >> gpurun_out/r2_tests.log
