@@ -748,14 +748,17 @@ def reference_python_report(torch):
     into baseline/_ref (pip, from a copy of /root/reference/pkg), timed on the
     box's host: generate -> detect_dependencies -> critical_path
     (taskgen.py:180-234, depgraph.py:102-174) on the cfg1 grid and on 32^3,
-    and executor.execute (executor.py:287-354) with W = all host cores on the
-    colour-order stream with the integer payload; beside each, the same
-    pipeline / execution on the device."""
+    executor.execute (executor.py:287-354) with W = all host cores on the
+    colour-order stream with the integer payload, and simulate /
+    simulate_dynamic (schedsim.py:63-163) on the paper's 30x10x10 domain;
+    beside each, the same pipeline / execution / schedule on the device."""
     ref = os.path.join(ROOT, "baseline", "_ref")
     if not os.path.isdir(os.path.join(ref, "cellsched")):
         return {"unavailable": "baseline/_ref not installed (pip install of /root/reference/pkg)"}
     if ref not in sys.path:
         sys.path.insert(0, ref)
+    import numpy as np
+
     import cellsched as R
     from cellsched import executor as RX
 
@@ -807,6 +810,39 @@ def reference_python_report(torch):
             "device_note": "wall clock incl. host interning of the Task objects and edge detection",
             "device_conflicts": conflicts,
             "accumulators_equal": res.accumulators == acc}
+    # the worker-pool model (schedsim.py:63-163) on the paper's 3D domain: the
+    # reference's simulate / simulate_dynamic vs the device list scheduler
+    from cellsched import schedsim as RS
+    from paper_1401_4441_b200 import depgraph as MD, schedsim as MS
+
+    g = R.GridSpec((30, 10, 10))
+    rg = R.detect_dependencies(R.generate_basic(g, R.order_with_displacement(3, 1)))
+    mg = MD.detect_dependencies(taskgen.generate_basic(GridSpec((30, 10, 10)), taskgen.order_with_displacement(3, 1)))
+    sim = {}
+    for W in (8, 16):
+        t0 = time.perf_counter()
+        rr = RS.simulate(rg, RS.SimConfig(W))
+        t1 = time.perf_counter()
+        MS.simulate(mg, MS.SimConfig(W))  # warm-up
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        e = np.asarray(mg.edges, np.int64)
+        start, mk = MS.simulate_edges(mg.task_count, e[:, 0], e[:, 1], W)
+        t3 = time.perf_counter()
+        sim[f"delta1_W{W}"] = {"tasks": rg.task_count, "makespan": rr.makespan, "device_makespan": mk,
+                               "speedup": rr.speedup, "reference_s": t1 - t0, "device_ms": 1e3 * (t3 - t2)}
+    plan_r, plan_m = R.NestedPlan(g), taskgen.NestedPlan(GridSpec((30, 10, 10)))
+    t0 = time.perf_counter()
+    rn = RS.simulate_dynamic(plan_r, RS.SimConfig(32))
+    t1 = time.perf_counter()
+    MS.nested_device(plan_m, 32)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    _, mkn = MS.nested_device(plan_m, 32)
+    t3 = time.perf_counter()
+    sim["nested_W32"] = {"tasks": len(rn.graph.tasks), "makespan": rn.makespan, "device_makespan": mkn,
+                         "speedup": rn.speedup, "reference_s": t1 - t0, "device_ms": 1e3 * (t3 - t2)}
+    out["simulate"] = sim
     out["note"] = ("reference Python, single process (the executor's worker threads share the GIL); "
                    "device = this package's stream generator + detector + depth (wall clock incl. allocations) "
                    "and its ready-queue DAG runtime (cs_dag_execute) with the same payload")

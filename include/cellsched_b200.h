@@ -352,11 +352,13 @@ int cs_set_ghost_plane(const cs_box *b, int64_t n_owned, const int32_t *ghost_co
  * ascending id order.  Both synchronise (the makespan is returned on the host). */
 /* simulate (schedsim.py:63-90): successor CSR sptr[ntasks+1] / succ[nedges] of
  * a forward-edge graph; start[t] = time step task t runs; *makespan_host =
- * SimResult.makespan.  CS_ECYCLE if the schedule stalls (schedsim.py:88-89). */
+ * SimResult.makespan.  CS_ECYCLE if the schedule stalls (schedsim.py:88-89).
+ * max_indegree_host: the largest predecessor count (graphs up to 180,000
+ * tasks with indegrees <= 255 keep the ready set in shared memory). */
 size_t cs_listsched_ws_bytes(int64_t ntasks);
 int cs_simulate_static(int64_t ntasks, int64_t nedges, const int64_t *sptr, const int32_t *succ,
-                       int64_t workers, int32_t *start, int64_t *makespan_host, void *ws,
-                       size_t ws_bytes, void *stream);
+                       int64_t workers, int64_t max_indegree_host, int32_t *start,
+                       int64_t *makespan_host, void *ws, size_t ws_bytes, void *stream);
 /* simulate_dynamic on a NestedPlan (schedsim.py:93-163, taskgen.py:279-325):
  * order_host = n offsets x dim int8, intra first.  Task arrays (capacity >=
  * cells * n): home cell, chain entry (index into order), spawning parent (-1 =

@@ -111,7 +111,7 @@ _SIGS = {
     "cs_dag_ws_bytes": (_SZ, [_I64, _I64]),
     "cs_dag_execute": (C.c_int, [_I64, C.c_int] + [_P] * 9 + [_I64, _P, _P, _P, _I64, _P, C.c_int, _P, _P, _SZ, _P]),
     "cs_listsched_ws_bytes": (_SZ, [_I64]),
-    "cs_simulate_static": (C.c_int, [_I64, _I64, _P, _P, _I64, _P, _P, _P, _SZ, _P]),
+    "cs_simulate_static": (C.c_int, [_I64, _I64, _P, _P, _I64, _I64, _P, _P, _P, _SZ, _P]),
     "cs_nested_ws_bytes": (_SZ, [_P, C.c_int]),
     "cs_simulate_nested": (C.c_int, [_P, _P, C.c_int, _I64] + [_P] * 6 + [_I64, _P, _P, _P, _SZ, _P]),
     "cs_slab_ws_bytes": (_SZ, [_I64]),

@@ -57,13 +57,15 @@ __device__ __forceinline__ int ls_block_scan(int v, int *wsum, int &total) {
 }
 
 // the first `need` set bits at or after word `cursor` go to batch[]; their
-// bits are cleared.  Returns the number taken (all threads).
+// bits are cleared.  Returns the number taken (all threads).  SMEM: the
+// bitmap lives in shared memory (else in global memory, changed by atomics).
+template <bool SMEM = false>
 __device__ int ls_select(uint32_t *bits, int64_t nwords, int64_t cursor, int64_t need,
                          int32_t *batch, int *wsum) {
   int64_t got = 0;
   for (int64_t w0 = cursor; w0 < nwords && got < need; w0 += LS_THREADS) {
     const int64_t w = w0 + threadIdx.x;
-    uint32_t word = w < nwords ? __ldcg(bits + w) : 0u;  // bits also change by atomics
+    uint32_t word = w < nwords ? (SMEM ? bits[w] : __ldcg(bits + w)) : 0u;  // (atomics change bits)
     int total;
     const int before = ls_block_scan(__popc(word), wsum, total);
     const int64_t left = need - got;
@@ -76,7 +78,8 @@ __device__ int ls_select(uint32_t *bits, int64_t nwords, int64_t cursor, int64_t
         batch[got + r] = (int32_t)(w * 32 + b);
         ++r;
       }
-      __stcg(bits + w, keep);  // taken bits cleared; this thread owns word w
+      if (SMEM) bits[w] = keep;  // taken bits cleared; this thread owns word w
+      else __stcg(bits + w, keep);
     }
     got += total < left ? total : left;
   }
@@ -118,6 +121,58 @@ __global__ void __launch_bounds__(LS_THREADS, 1)
   }
 }
 
+// The same schedule with the ready bitmap and 8-bit indegrees in shared
+// memory (graphs of up to LS_SMEM_TASKS tasks whose indegrees fit a byte):
+// a time step then costs a few barriers instead of L2 round trips.
+#define LS_SMEM_TASKS 180000  // 1.125 bytes per task of shared memory
+__global__ void __launch_bounds__(LS_THREADS, 1)
+    k_ls_static_smem(int64_t n, const int64_t *__restrict__ sptr, const int32_t *__restrict__ succ,
+                     int64_t W, const int32_t *indeg_g, const uint32_t *bits_g, int32_t *batch,
+                     int32_t *start, LsState *st) {
+  extern __shared__ __align__(16) unsigned char ls_raw[];
+  const int64_t nwords = (n + 31) / 32;
+  uint32_t *bits = reinterpret_cast<uint32_t *>(ls_raw);
+  unsigned *indeg = reinterpret_cast<unsigned *>(ls_raw + 4 * nwords);  // 4 tasks per word
+  __shared__ int wsum[32];
+  __shared__ int64_t s_cursor;
+  for (int64_t w = threadIdx.x; w < nwords; w += LS_THREADS) bits[w] = bits_g[w];
+  for (int64_t q = threadIdx.x; q < (n + 3) / 4; q += LS_THREADS) {
+    unsigned v = 0;
+    for (int k = 0; k < 4; ++k)
+      if (4 * q + k < n) v |= (unsigned)indeg_g[4 * q + k] << (8 * k);
+    indeg[q] = v;
+  }
+  __syncthreads();
+  int64_t now = 0, done = 0, cursor = 0;
+  while (true) {
+    const int got = ls_select<true>(bits, nwords, cursor, W, batch, wsum);
+    if (got == 0) break;
+    for (int k = threadIdx.x; k < got; k += LS_THREADS) {
+      const int32_t t = batch[k];
+      start[t] = (int32_t)now;
+      for (int64_t s = sptr[t]; s < sptr[t + 1]; ++s) {
+        const int32_t v = succ[s];
+        const unsigned sh = 8u * (v & 3);
+        // bytes of one word never borrow from each other: an indegree only
+        // reaches zero, never goes below it
+        const unsigned old = atomicSub(&indeg[v >> 2], 1u << sh);
+        if (((old >> sh) & 0xFFu) == 1u) atomicOr(&bits[v >> 5], 1u << (v & 31));
+      }
+    }
+    if (threadIdx.x == 0) s_cursor = batch[0] >> 5;
+    __syncthreads();
+    cursor = s_cursor;
+    ++now;
+    done += got;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->now = now;
+    st->done = done;
+    st->ntasks = n;
+  }
+}
+
 __global__ void k_ls_static_init(int64_t n, const int64_t *__restrict__ sptr,
                                  const int32_t *__restrict__ succ, int32_t *indeg) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < sptr[n];
@@ -142,8 +197,8 @@ size_t cs_listsched_ws_bytes(int64_t ntasks) {
 }
 
 int cs_simulate_static(int64_t ntasks, int64_t nedges, const int64_t *sptr, const int32_t *succ,
-                       int64_t workers, int32_t *start, int64_t *makespan_host, void *ws,
-                       size_t ws_bytes, void *stream) {
+                       int64_t workers, int64_t max_indegree_host, int32_t *start,
+                       int64_t *makespan_host, void *ws, size_t ws_bytes, void *stream) {
   CS_REQUIRE(ntasks >= 1, "cannot simulate an empty graph");
   CS_REQUIRE(workers >= 1, "workers must be >= 1, got %lld", (long long)workers);
   CS_REQUIRE(ntasks < (1ll << 31), "simulate: at most 2^31-1 tasks");
@@ -159,7 +214,19 @@ int cs_simulate_static(int64_t ntasks, int64_t nedges, const int64_t *sptr, cons
     k_ls_static_init<<<592, 256, 0, s>>>(ntasks, sptr, succ, indeg);
   const int64_t nwords = (ntasks + 31) / 32;
   k_ls_roots<<<(unsigned)((nwords + 255) / 256), 256, 0, s>>>(ntasks, indeg, bits);
-  k_ls_static<<<1, LS_THREADS, 0, s>>>(ntasks, sptr, succ, W, indeg, bits, batch, start, st);
+  const size_t smem = 4 * (size_t)nwords + 4 * (size_t)((ntasks + 3) / 4);
+  if (ntasks <= LS_SMEM_TASKS && max_indegree_host <= 255) {
+    static size_t attr_smem[CS_MAX_DEVICES];
+    const int dev = cs_device_index();
+    if (smem > attr_smem[dev]) {
+      CS_CUDA(cudaFuncSetAttribute(k_ls_static_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      attr_smem[dev] = smem;
+    }
+    k_ls_static_smem<<<1, LS_THREADS, smem, s>>>(ntasks, sptr, succ, W, indeg, bits, batch, start, st);
+  } else {
+    k_ls_static<<<1, LS_THREADS, 0, s>>>(ntasks, sptr, succ, W, indeg, bits, batch, start, st);
+  }
   CS_TRY(cs_check_launch("k_ls_static"));
   LsState h;
   CS_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -109,9 +109,10 @@ def simulate_edges(ntasks: int, eu, ev, workers: int):
     wsb = _lib.load().cs_listsched_ws_bytes(ntasks)
     ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
     mk = C.c_int64()
+    maxdeg = int(np.bincount(ev, minlength=1).max()) if len(ev) else 0
     st = _lib.load().cs_simulate_static(ntasks, len(succ), _lib.ptr(d_sptr), _lib.ptr(d_succ),
-                                         int(workers), _lib.ptr(start), C.byref(mk), _lib.ptr(ws),
-                                         wsb, _lib.stream_handle())
+                                         int(workers), maxdeg, _lib.ptr(start), C.byref(mk),
+                                         _lib.ptr(ws), wsb, _lib.stream_handle())
     if st == _lib.CS_ECYCLE:
         raise RuntimeError(_lib.load().cs_last_error().decode())
     _lib.check(st, "cs_simulate_static")
