@@ -121,52 +121,95 @@ __global__ void __launch_bounds__(LS_THREADS, 1)
   }
 }
 
-// The same schedule with the ready bitmap and 8-bit indegrees in shared
-// memory (graphs of up to LS_SMEM_TASKS tasks whose indegrees fit a byte):
-// a time step then costs a few barriers instead of L2 round trips.
+// The same schedule run by ONE warp with the ready bitmap and 8-bit
+// indegrees in shared memory (graphs of up to LS_SMEM_TASKS tasks whose
+// indegrees fit a byte): a time step is a warp ballot scan of the bitmap and
+// a warp-wide release, synchronised by __syncwarp only -- its cost is the
+// global-memory lookups of the batch's successors.
 #define LS_SMEM_TASKS 180000  // 1.125 bytes per task of shared memory
-__global__ void __launch_bounds__(LS_THREADS, 1)
-    k_ls_static_smem(int64_t n, const int64_t *__restrict__ sptr, const int32_t *__restrict__ succ,
+__global__ void __launch_bounds__(32, 1)
+    k_ls_static_warp(int64_t n, const int64_t *__restrict__ sptr, const int32_t *__restrict__ succ,
                      int64_t W, const int32_t *indeg_g, const uint32_t *bits_g, int32_t *batch,
                      int32_t *start, LsState *st) {
   extern __shared__ __align__(16) unsigned char ls_raw[];
+  const int lane = threadIdx.x;
   const int64_t nwords = (n + 31) / 32;
   uint32_t *bits = reinterpret_cast<uint32_t *>(ls_raw);
   unsigned *indeg = reinterpret_cast<unsigned *>(ls_raw + 4 * nwords);  // 4 tasks per word
-  __shared__ int wsum[32];
-  __shared__ int64_t s_cursor;
-  for (int64_t w = threadIdx.x; w < nwords; w += LS_THREADS) bits[w] = bits_g[w];
-  for (int64_t q = threadIdx.x; q < (n + 3) / 4; q += LS_THREADS) {
+  // highest bitmap word that may hold a ready bit: the scan stops there (a
+  // ready set smaller than W would otherwise scan to the end every step)
+  __shared__ int64_t s_hiw;
+  int64_t hiw = 0;
+  for (int64_t w = lane; w < nwords; w += 32) {
+    bits[w] = bits_g[w];
+    if (bits_g[w]) hiw = w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hiw = max(hiw, __shfl_xor_sync(CS_FULL, hiw, o));
+  if (lane == 0) s_hiw = hiw;
+  for (int64_t q = lane; q < (n + 3) / 4; q += 32) {
     unsigned v = 0;
     for (int k = 0; k < 4; ++k)
       if (4 * q + k < n) v |= (unsigned)indeg_g[4 * q + k] << (8 * k);
     indeg[q] = v;
   }
-  __syncthreads();
+  __syncwarp();
   int64_t now = 0, done = 0, cursor = 0;
   while (true) {
-    const int got = ls_select<true>(bits, nwords, cursor, W, batch, wsum);
+    // select: the first W set bits from word `cursor` on, 32 words per pass
+    int64_t got = 0;
+    const int64_t wend = min(nwords, *(volatile int64_t *)&s_hiw + 1);
+    for (int64_t w0 = cursor; w0 < wend && got < W; w0 += 32) {
+      const int64_t w = w0 + lane;
+      uint32_t word = w < wend ? bits[w] : 0u;
+      const int c = __popc(word);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(CS_FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(CS_FULL, incl, 31);
+      const int64_t left = W - got;
+      int64_t r = incl - c;
+      if (word && r < left) {
+        uint32_t keep = word;
+        while (keep && r < left) {
+          const int b = __ffs(keep) - 1;
+          keep &= keep - 1;
+          batch[got + r] = (int32_t)(w * 32 + b);
+          ++r;
+        }
+        bits[w] = keep;
+      }
+      got += total < left ? total : left;
+    }
+    __syncwarp();
     if (got == 0) break;
-    for (int k = threadIdx.x; k < got; k += LS_THREADS) {
+    // release: start step, successors' indegrees, newly ready bits
+    for (int64_t k = lane; k < got; k += 32) {
       const int32_t t = batch[k];
       start[t] = (int32_t)now;
-      for (int64_t s = sptr[t]; s < sptr[t + 1]; ++s) {
+      const int64_t s1 = sptr[t + 1];
+      for (int64_t s = sptr[t]; s < s1; ++s) {
         const int32_t v = succ[s];
         const unsigned sh = 8u * (v & 3);
         // bytes of one word never borrow from each other: an indegree only
         // reaches zero, never goes below it
         const unsigned old = atomicSub(&indeg[v >> 2], 1u << sh);
-        if (((old >> sh) & 0xFFu) == 1u) atomicOr(&bits[v >> 5], 1u << (v & 31));
+        if (((old >> sh) & 0xFFu) == 1u) {
+          atomicOr(&bits[v >> 5], 1u << (v & 31));
+          atomicMax((unsigned long long *)&s_hiw, (unsigned long long)(v >> 5));
+        }
       }
     }
-    if (threadIdx.x == 0) s_cursor = batch[0] >> 5;
-    __syncthreads();
-    cursor = s_cursor;
+    __syncwarp();
+    cursor = __shfl_sync(CS_FULL, lane == 0 ? (int64_t)(batch[0] >> 5) : (int64_t)0, 0);
     ++now;
     done += got;
-    __syncthreads();
+    __syncwarp();
   }
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     st->now = now;
     st->done = done;
     st->ntasks = n;
@@ -219,11 +262,11 @@ int cs_simulate_static(int64_t ntasks, int64_t nedges, const int64_t *sptr, cons
     static size_t attr_smem[CS_MAX_DEVICES];
     const int dev = cs_device_index();
     if (smem > attr_smem[dev]) {
-      CS_CUDA(cudaFuncSetAttribute(k_ls_static_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      CS_CUDA(cudaFuncSetAttribute(k_ls_static_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       attr_smem[dev] = smem;
     }
-    k_ls_static_smem<<<1, LS_THREADS, smem, s>>>(ntasks, sptr, succ, W, indeg, bits, batch, start, st);
+    k_ls_static_warp<<<1, 32, smem, s>>>(ntasks, sptr, succ, W, indeg, bits, batch, start, st);
   } else {
     k_ls_static<<<1, LS_THREADS, 0, s>>>(ntasks, sptr, succ, W, indeg, bits, batch, start, st);
   }
